@@ -72,23 +72,23 @@ def backproject(geom, sino: np.ndarray, pixels=None) -> np.ndarray:
     else:
         X1, X2 = xs[np.asarray(pixels[0])], xs[np.asarray(pixels[1])]
     b = np.zeros(X1.shape)
-    ym_all = g.lambda_y * (np.arange(-H_CORR, M + H_CORR) - (M // 2))
     for it, t in enumerate(g.angles):
         d = interpolation_degree(g, t)
-        gt = corrected_row(np.asarray(sino[it], dtype=np.float64), d)
+        gt = corrected_row(np.asarray(sino[it], dtype=np.float64), d)   # index j <-> m = j - h
         w = bp_widths(g, t)
         half = 0.5 * sum(kept_widths(w))
         kt = -np.sin(t) * X1 + np.cos(t) * X2
-        # only samples with |y_m - k_theta| < half contribute (M is 0 outside its support)
-        lo = np.floor((kt.min() - half) / g.lambda_y) + (M // 2) + H_CORR
-        hi = np.ceil((kt.max() + half) / g.lambda_y) + (M // 2) + H_CORR
-        for mi in range(int(max(lo, 0)), int(min(hi, M + 2 * H_CORR - 1)) + 1):
-            if gt[mi] == 0.0:
-                continue
-            arg = ym_all[mi] - kt
-            msk = np.abs(arg) < half
-            if msk.any():
-                b[msk] += g.lambda_x ** 2 * g.lambda_y * gt[mi] * box_spline(w, arg[msk])
+        # only samples with |y_m - k_theta| < half contribute (M is 0 outside its support):
+        # for each pixel the S consecutive detector indices starting at m_first
+        S = int(np.floor(2.0 * half / g.lambda_y)) + 2
+        m_first = np.floor((kt - half) / g.lambda_y + (M // 2)).astype(np.int64)
+        m = m_first[..., None] + np.arange(S)
+        arg = g.lambda_y * (m - (M // 2)) - kt[..., None]
+        j = m + H_CORR
+        ok = (np.abs(arg) < half) & (j >= 0) & (j < M + 2 * H_CORR)
+        vals = np.zeros(arg.shape)
+        vals[ok] = gt[j[ok]] * box_spline(w, arg[ok])
+        b += g.lambda_x ** 2 * g.lambda_y * vals.sum(axis=-1)
     return b
 
 

@@ -55,6 +55,23 @@ def gram_taps(geom, angle_begin: int = 0, angle_end: int | None = None) -> np.nd
     return G
 
 
+def gram_taps_at(geom, dk1, dk2) -> np.ndarray:
+    """The same sum as gram_taps at selected offsets (dk1[i], dk2[i]) -- for sampling
+    full-size filters one tap at a time."""
+    g = as_geometry(geom)
+    lam = g.lambda_x
+    a = np.asarray(dk1, dtype=np.float64)
+    b = np.asarray(dk2, dtype=np.float64)
+    out = np.zeros(a.shape, dtype=np.float64)
+    for t in g.angles:
+        w = gram_widths(lam, t, g.zeta)
+        half = 0.5 * sum(kept_widths(w))
+        u = lam * (-np.sin(t) * a + np.cos(t) * b)
+        m = np.abs(u) < half
+        out[m] += lam ** 4 * box_spline(w, u[m])
+    return out
+
+
 def toeplitz_matrix(taps: np.ndarray) -> np.ndarray:
     """Dense N^2 x N^2 matrix G[i, j] = taps[k_i - k_j], row-major pixel order."""
     N = (taps.shape[0] + 1) // 2

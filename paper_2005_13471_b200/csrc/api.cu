@@ -1,0 +1,503 @@
+// api.cu -- the C ABI of include/bsct.h: validation, plans, launch sequencing.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/bsct.h"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+using namespace bsct;
+
+namespace {
+
+thread_local std::string g_err;
+
+bsct_status fail(bsct_status st, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CU(expr)                                                                        \
+  do {                                                                                  \
+    cudaError_t e_ = (expr);                                                            \
+    if (e_ != cudaSuccess)                                                              \
+      return fail(e_ == cudaErrorMemoryAllocation ? BSCT_ENOMEM : BSCT_ECUDA, "%s: %s (%s:%d)", #expr, \
+                  cudaGetErrorString(e_), __FILE__, __LINE__);                          \
+  } while (0)
+
+constexpr int HC = 25;
+
+int fft_size(int N) {
+  int L = 2;
+  while (L < 2 * N - 1) L *= 2;
+  return L;
+}
+
+bsct_status validate(const bsct_geometry *g, bsct_dtype dt) {
+  if (!g) return fail(BSCT_EINVAL, "geometry is NULL");
+  if (g->N < 1 || g->N > 2048) return fail(BSCT_EINVAL, "N = %d outside [1, 2048]", g->N);
+  if (dt != BSCT_F32 && dt != BSCT_F64) return fail(BSCT_EINVAL, "unknown dtype %d", (int)dt);
+  if (dt == BSCT_F64 && g->N > 1024) return fail(BSCT_EINVAL, "FP64 plans support N <= 1024 (got %d)", g->N);
+  if (!(g->lambda_x > 0) || !std::isfinite(g->lambda_x)) return fail(BSCT_EINVAL, "lambda_x must be > 0");
+  if (!(g->lambda_y > 0) || !std::isfinite(g->lambda_y)) return fail(BSCT_EINVAL, "lambda_y must be > 0");
+  if (!(g->zeta_blur >= 0) || !std::isfinite(g->zeta_blur)) return fail(BSCT_EINVAL, "zeta_blur must be >= 0");
+  if (g->n_angles < 1 || g->n_angles > 65535) return fail(BSCT_EINVAL, "n_angles = %d outside [1, 65535]", g->n_angles);
+  if (g->n_det < 1 || g->n_det > (1 << 20)) return fail(BSCT_EINVAL, "n_det = %d outside [1, 2^20]", g->n_det);
+  if (!g->angles) return fail(BSCT_EINVAL, "angles is NULL");
+  for (int i = 0; i < g->n_angles; ++i)
+    if (!std::isfinite(g->angles[i])) return fail(BSCT_EINVAL, "angle %d is not finite", i);
+  return BSCT_OK;
+}
+
+template <typename T>
+size_t tables_bytes(int n) { return PPTables<T>::bytes(n); }
+
+}  // namespace
+
+struct bsct_plan_s {
+  int N = 0, L = 0, n_angles = 0, M = 0, max_batch = 0;
+  double lx = 1, ly = 1, zeta = 0;
+  bsct_dtype dt = BSCT_F32;
+  double *angles = nullptr;
+  void *bp_mem = nullptr, *fw_mem = nullptr;
+  void *S = nullptr, *tw = nullptr, *spec_work = nullptr;
+  void *T1 = nullptr, *gt = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
+  void *sino_dev = nullptr, *b_dev = nullptr, *x_dev = nullptr;  // reconstruct_host staging
+  double *alpha = nullptr, *gpart = nullptr, *rpart = nullptr, *tau = nullptr;
+  double *rho = nullptr;
+  int rho_iters = -1;
+  int *flags = nullptr;
+  int64_t launches = 0;
+  // kernel-class profiler: CUDA events bracket every launch on the caller's stream
+  bool prof_on = false;
+  std::vector<cudaEvent_t> prof_pool;
+  std::vector<std::pair<int, size_t>> prof_marks;  // (class, index of the start event)
+  size_t prof_used = 0;
+  double prof_ms[BSCT_K_COUNT] = {};
+  int64_t prof_cnt[BSCT_K_COUNT] = {};
+  size_t esize() const { return dt == BSCT_F64 ? 8 : 4; }
+};
+
+namespace {
+
+template <typename T>
+PPTables<T> tables_of(void *mem, int n) {
+  PPTables<T> t;
+  t.carve(mem, n);
+  return t;
+}
+
+cudaError_t prof_begin(bsct_plan p, int cls, cudaStream_t s) {
+  if (!p->prof_on) return cudaSuccess;
+  while (p->prof_pool.size() < p->prof_used + 2) {
+    cudaEvent_t e;
+    cudaError_t err = cudaEventCreate(&e);
+    if (err != cudaSuccess) return err;
+    p->prof_pool.push_back(e);
+  }
+  p->prof_marks.push_back({cls, p->prof_used});
+  cudaError_t err = cudaEventRecord(p->prof_pool[p->prof_used], s);
+  p->prof_used += 2;
+  return err;
+}
+
+cudaError_t prof_end(bsct_plan p, cudaStream_t s) {
+  if (!p->prof_on) return cudaSuccess;
+  return cudaEventRecord(p->prof_pool[p->prof_marks.back().second + 1], s);
+}
+
+// one library launcher call (nk kernels) of kernel class `cls`, bracketed by profiler events
+#define LAUNCH(p, cls, nk, expr)    \
+  do {                              \
+    CU(prof_begin((p), (cls), s));  \
+    CU(expr);                       \
+    CU(prof_end((p), s));           \
+    (p)->launches += (nk);          \
+  } while (0)
+
+bsct_status check_plan(bsct_plan p, int B) {
+  if (!p) return fail(BSCT_EINVAL, "plan is NULL");
+  if (B < 0) return fail(BSCT_EINVAL, "batch %d < 0", B);
+  if (B > p->max_batch) return fail(BSCT_ESHAPE, "batch %d exceeds the plan's max_batch %d", B, p->max_batch);
+  return BSCT_OK;
+}
+
+template <int L>
+void twiddles_L(std::vector<double> &re, std::vector<double> &im) {
+  re.assign(FftCfg<L>::TW_SIZE + 1, 0.0);
+  im.assign(FftCfg<L>::TW_SIZE + 1, 0.0);
+  fft_twiddles_host<L>(re.data(), im.data());
+}
+
+void twiddles(int L, std::vector<double> &re, std::vector<double> &im) {
+  switch (L) {
+    case 2: twiddles_L<2>(re, im); break;
+    case 4: twiddles_L<4>(re, im); break;
+    case 8: twiddles_L<8>(re, im); break;
+    case 16: twiddles_L<16>(re, im); break;
+    case 32: twiddles_L<32>(re, im); break;
+    case 64: twiddles_L<64>(re, im); break;
+    case 128: twiddles_L<128>(re, im); break;
+    case 256: twiddles_L<256>(re, im); break;
+    case 512: twiddles_L<512>(re, im); break;
+    case 1024: twiddles_L<1024>(re, im); break;
+    case 2048: twiddles_L<2048>(re, im); break;
+    case 4096: twiddles_L<4096>(re, im); break;
+  }
+}
+
+template <typename T>
+bsct_status gram_build_t(const bsct_geometry *g, int a0, int a1, T *taps, cudaStream_t s) {
+  const int n = a1 - a0;
+  const int N = g->N;
+  const size_t D2 = (size_t)(2 * N - 1) * (2 * N - 1);
+  if (n == 0) {
+    CU(cudaMemsetAsync(taps, 0, D2 * sizeof(T), s));
+    return BSCT_OK;
+  }
+  double *ang = nullptr;
+  void *mem = nullptr;
+  CU(cudaMallocAsync((void **)&ang, sizeof(double) * n, s));
+  CU(cudaMallocAsync(&mem, tables_bytes<T>(n), s));
+  CU(cudaMemcpyAsync(ang, g->angles + a0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
+  PPTables<T> tb = tables_of<T>(mem, n);
+  CU(build_pp_tables<T>(ang, n, PP_GRAM, g->lambda_x, g->lambda_y, g->zeta_blur, tb, s));
+  CU(gram_taps<T>(N, g->lambda_x, n, tb.cs, tb.view(), taps, s));
+  CU(cudaFreeAsync(mem, s));
+  CU(cudaFreeAsync(ang, s));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status plan_filter_t(bsct_plan p, const void *taps, cudaStream_t s) {
+  const int N = p->N, L = p->L, n = p->n_angles;
+  PPTables<T> bp = tables_of<T>(p->bp_mem, n), fw = tables_of<T>(p->fw_mem, n);
+  LAUNCH(p, BSCT_K_TABLES, 1, (build_pp_tables<T>(p->angles, n, PP_BP, p->lx, p->ly, p->zeta, bp, s)));
+  LAUNCH(p, BSCT_K_TABLES, 1, (build_pp_tables<T>(p->angles, n, PP_FWD, p->lx, p->ly, p->zeta, fw, s)));
+  LAUNCH(p, BSCT_K_SPECTRUM, 2,
+         (filter_spectrum<T>(N, L, (const T *)taps, (T *)p->S, (cplx<T> *)p->spec_work, (const cplx<T> *)p->tw, s)));
+  LAUNCH(p, BSCT_K_SPECTRUM, 2, (spectrum_max<T>(L, (const T *)p->S, p->tau, s)));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
+  const int N = p->N, L = p->L, n = p->n_angles, M = p->M, Bm = p->max_batch;
+  const size_t Q = L / 2 + 1;
+  CU(cudaMalloc(&p->bp_mem, tables_bytes<T>(n)));
+  CU(cudaMalloc(&p->fw_mem, tables_bytes<T>(n)));
+  // FFT twiddles
+  std::vector<double> re, im;
+  twiddles(L, re, im);
+  std::vector<cplx<T>> twh(re.size());
+  for (size_t i = 0; i < re.size(); ++i) twh[i] = cplx<T>{(T)re[i], (T)im[i]};
+  CU(cudaMalloc(&p->tw, sizeof(cplx<T>) * twh.size()));
+  CU(cudaMemcpyAsync(p->tw, twh.data(), sizeof(cplx<T>) * twh.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMalloc(&p->S, sizeof(T) * Q * L));
+  CU(cudaMalloc(&p->spec_work, sizeof(cplx<T>) * Q * L));
+  CU(cudaMalloc((void **)&p->tau, sizeof(double)));
+  bsct_status st = plan_filter_t<T>(p, taps, s);
+  if (st != BSCT_OK) return st;
+  // workspaces
+  const size_t nn = (size_t)N * N;
+  const size_t Bz = Bm > 0 ? Bm : 1;
+  CU(cudaMalloc(&p->T1, sizeof(cplx<T>) * Q * N * Bz));
+  CU(cudaMalloc(&p->gt, sizeof(T) * (size_t)n * (M + 2 * HC) * Bz));
+  CU(cudaMalloc(&p->r, sizeof(T) * nn * Bz));
+  CU(cudaMalloc(&p->p, sizeof(T) * nn * Bz));
+  CU(cudaMalloc(&p->q, sizeof(T) * nn * Bz));
+  CU(cudaMalloc((void **)&p->alpha, sizeof(double) * Bz));
+  CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * pass_b_blocks(L)));
+  CU(cudaMalloc((void **)&p->rpart, sizeof(double) * Bz * vec_blocks(N)));
+  CU(cudaMalloc((void **)&p->flags, sizeof(int) * Bz));
+  CU(cudaStreamSynchronize(s));
+  return BSCT_OK;
+}
+
+SolverWork solver_work(bsct_plan p, double *resid, int *flags) {
+  SolverWork w;
+  w.rho = p->rho;
+  w.alpha = p->alpha;
+  w.gpart = p->gpart;
+  w.gstride = pass_b_blocks(p->L);
+  w.rpart = p->rpart;
+  w.rstride = vec_blocks(p->N);
+  w.flags = flags ? flags : p->flags;
+  w.resid = resid;
+  w.tau = p->tau;
+  return w;
+}
+
+template <typename T>
+bsct_status normal_apply_t(bsct_plan p, const T *x, T *y, int B, double *gpart, cudaStream_t s) {
+  auto *T1 = (cplx<T> *)p->T1;
+  auto *tw = (const cplx<T> *)p->tw;
+  LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, B, x, T1, tw, s)));
+  LAUNCH(p, BSCT_K_PASS_B, 1, (pass_b<T>(p->N, p->L, B, T1, (const T *)p->S, tw, gpart, s)));
+  LAUNCH(p, BSCT_K_PASS_C, 1, (pass_c<T>(p->N, p->L, B, T1, y, tw, s)));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t s) {
+  PPTables<T> bp = tables_of<T>(p->bp_mem, p->n_angles);
+  LAUNCH(p, BSCT_K_CORRECTION, 1, (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s)));
+  LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+         (backproject<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, bp.cs, bp.view(), (const T *)p->gt, b, s)));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver, double *resid, int *flags,
+                    cudaStream_t s) {
+  if (p->rho_iters < iters) {
+    if (p->rho) CU(cudaFree(p->rho));
+    p->rho = nullptr;
+    CU(cudaMalloc((void **)&p->rho, sizeof(double) * (size_t)(iters + 1) * (p->max_batch > 0 ? p->max_batch : 1)));
+    p->rho_iters = iters;
+  }
+  SolverWork w = solver_work(p, resid, flags);
+  // rho rows have stride (iters + 1): the kernels index rho[b * (iters+1) + k]
+  T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
+  LAUNCH(p, BSCT_K_SOLVER_INIT, 2, (solver_init<T>(p->N, B, b, x, r, solver == BSCT_CG ? pp : (T *)nullptr, w, iters, s)));
+  for (int it = 0; it < iters; ++it) {
+    const T *d = solver == BSCT_CG ? pp : r;
+    bsct_status st = normal_apply_t<T>(p, d, q, B, solver == BSCT_LANDWEBER ? nullptr : p->gpart, s);
+    if (st != BSCT_OK) return st;
+    LAUNCH(p, BSCT_K_SOLVER_UPDATE, 1, (solver_update<T>(p->N, B, solver, it, iters, x, r, pp, q, w, s)));
+    LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (solver_finish<T>(p->N, B, solver, it, iters, r, pp, w, s)));
+  }
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status forward_t(bsct_plan p, const T *c, T *sino, int B, cudaStream_t s) {
+  PPTables<T> fw = tables_of<T>(p->fw_mem, p->n_angles);
+  LAUNCH(p, BSCT_K_FORWARD, 1, (forward_project<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, fw.cs, fw.view(), c, sino, s)));
+  return BSCT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t bsct_version(void) { return 100; }
+
+const char *bsct_last_error(void) { return g_err.c_str(); }
+
+int32_t bsct_fft_size(int32_t N) { return N < 1 ? 0 : fft_size(N); }
+
+bsct_status bsct_gram_build(const bsct_geometry *g, bsct_dtype dt, int32_t angle_begin, int32_t angle_end, void *taps,
+                            bsct_stream stream) {
+  bsct_status st = validate(g, dt);
+  if (st != BSCT_OK) return st;
+  if (angle_begin < 0 || angle_end < angle_begin || angle_end > g->n_angles)
+    return fail(BSCT_EINVAL, "angle range [%d, %d) not within [0, %d)", angle_begin, angle_end, g->n_angles);
+  if (!taps) return fail(BSCT_EINVAL, "taps is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  return dt == BSCT_F64 ? gram_build_t<double>(g, angle_begin, angle_end, (double *)taps, s)
+                        : gram_build_t<float>(g, angle_begin, angle_end, (float *)taps, s);
+}
+
+bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *taps, int32_t max_batch,
+                             bsct_plan *out, bsct_stream stream) {
+  if (!out) return fail(BSCT_EINVAL, "out is NULL");
+  *out = nullptr;
+  bsct_status st = validate(g, dt);
+  if (st != BSCT_OK) return st;
+  if (!taps) return fail(BSCT_EINVAL, "taps is NULL");
+  if (max_batch < 0) return fail(BSCT_EINVAL, "max_batch < 0");
+  bsct_plan p = new bsct_plan_s();
+  p->N = g->N;
+  p->L = fft_size(g->N);
+  p->n_angles = g->n_angles;
+  p->M = g->n_det;
+  p->lx = g->lambda_x;
+  p->ly = g->lambda_y;
+  p->zeta = g->zeta_blur;
+  p->dt = dt;
+  p->max_batch = max_batch;
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaError_t e = cudaMalloc((void **)&p->angles, sizeof(double) * g->n_angles);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(p->angles, g->angles, sizeof(double) * g->n_angles, cudaMemcpyHostToDevice, s);
+  if (e != cudaSuccess) {
+    bsct_plan_destroy(p);
+    return fail(BSCT_ECUDA, "angle upload: %s", cudaGetErrorString(e));
+  }
+  st = dt == BSCT_F64 ? plan_init_t<double>(p, taps, s) : plan_init_t<float>(p, taps, s);
+  if (st != BSCT_OK) {
+    std::string msg = g_err;
+    bsct_plan_destroy(p);
+    g_err = msg;
+    return st;
+  }
+  *out = p;
+  return BSCT_OK;
+}
+
+bsct_status bsct_plan_destroy(bsct_plan p) {
+  if (!p) return BSCT_OK;
+  void *bufs[] = {p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->r, p->p, p->q,
+                  p->sino_dev, p->b_dev, p->x_dev, p->spec_work, p->alpha, p->gpart, p->rpart, p->tau, p->rho, p->flags};
+  for (void *b : bufs)
+    if (b) cudaFree(b);
+  for (cudaEvent_t e : p->prof_pool) cudaEventDestroy(e);
+  delete p;
+  return BSCT_OK;
+}
+
+bsct_status bsct_plan_profile(bsct_plan p, int32_t enable) {
+  bsct_status st = check_plan(p, 0);
+  if (st != BSCT_OK) return st;
+  p->prof_on = enable != 0;
+  return BSCT_OK;
+}
+
+bsct_status bsct_plan_profile_read(bsct_plan p, double *ms, int64_t *count, int32_t n) {
+  bsct_status st = check_plan(p, 0);
+  if (st != BSCT_OK) return st;
+  if (!p->prof_marks.empty()) {
+    CU(cudaEventSynchronize(p->prof_pool[p->prof_marks.back().second + 1]));
+    for (auto &m : p->prof_marks) {
+      float t = 0;
+      CU(cudaEventElapsedTime(&t, p->prof_pool[m.second], p->prof_pool[m.second + 1]));
+      p->prof_ms[m.first] += t;
+      p->prof_cnt[m.first] += 1;
+    }
+    p->prof_marks.clear();
+    p->prof_used = 0;
+  }
+  for (int i = 0; i < n && i < BSCT_K_COUNT; ++i) {
+    if (ms) ms[i] = p->prof_ms[i];
+    if (count) count[i] = p->prof_cnt[i];
+  }
+  for (int i = 0; i < BSCT_K_COUNT; ++i) {
+    p->prof_ms[i] = 0;
+    p->prof_cnt[i] = 0;
+  }
+  return BSCT_OK;
+}
+
+bsct_status bsct_plan_set_filter(bsct_plan p, const void *taps, bsct_stream stream) {
+  bsct_status st = check_plan(p, 0);
+  if (st != BSCT_OK) return st;
+  if (!taps) return fail(BSCT_EINVAL, "taps is NULL");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? plan_filter_t<double>(p, taps, s) : plan_filter_t<float>(p, taps, s);
+}
+
+bsct_status bsct_plan_spectrum(bsct_plan p, void *out, bsct_stream stream) {
+  bsct_status st = check_plan(p, 0);
+  if (st != BSCT_OK) return st;
+  if (!out) return fail(BSCT_EINVAL, "out is NULL");
+  CU(cudaMemcpyAsync(out, p->S, p->esize() * (size_t)(p->L / 2 + 1) * p->L, cudaMemcpyDeviceToDevice,
+                     (cudaStream_t)stream));
+  return BSCT_OK;
+}
+
+bsct_status bsct_correction_filter(bsct_plan p, const void *sino, void *g_tilde, int32_t B, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (B == 0) return BSCT_OK;
+  if (!sino || !g_tilde) return fail(BSCT_EINVAL, "NULL buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  p->launches = 0;
+  if (p->dt == BSCT_F64) {
+    PPTables<double> bp = tables_of<double>(p->bp_mem, p->n_angles);
+    LAUNCH(p, BSCT_K_CORRECTION, 0,
+           (correction_filter<double>(p->n_angles, p->M, B, bp.degree, (const double *)sino, (double *)g_tilde, s)));
+  } else {
+    PPTables<float> bp = tables_of<float>(p->bp_mem, p->n_angles);
+    LAUNCH(p, BSCT_K_CORRECTION, 0,
+           (correction_filter<float>(p->n_angles, p->M, B, bp.degree, (const float *)sino, (float *)g_tilde, s)));
+  }
+  p->launches = 1;
+  return BSCT_OK;
+}
+
+bsct_status bsct_backproject(bsct_plan p, const void *sino, void *b, int32_t B, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (B == 0) return BSCT_OK;
+  if (!sino || !b) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? backproject_t<double>(p, (const double *)sino, (double *)b, B, s)
+                           : backproject_t<float>(p, (const float *)sino, (float *)b, B, s);
+}
+
+bsct_status bsct_normal_apply(bsct_plan p, const void *x, void *y, int32_t B, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (B == 0) return BSCT_OK;
+  if (!x || !y) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? normal_apply_t<double>(p, (const double *)x, (double *)y, B, nullptr, s)
+                           : normal_apply_t<float>(p, (const float *)x, (float *)y, B, nullptr, s);
+}
+
+bsct_status bsct_cg_solve(bsct_plan p, const void *b, void *x, int32_t B, int32_t iters, int32_t solver,
+                          double *resid_hist, int32_t *flags, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
+  if (solver < BSCT_CG || solver > BSCT_LANDWEBER) return fail(BSCT_EINVAL, "unknown solver %d", solver);
+  if (B == 0) return BSCT_OK;
+  if (!b || !x) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64
+             ? solve_t<double>(p, (const double *)b, (double *)x, B, iters, solver, resid_hist, flags, s)
+             : solve_t<float>(p, (const float *)b, (float *)x, B, iters, solver, resid_hist, flags, s);
+}
+
+bsct_status bsct_forward_project(bsct_plan p, const void *c, void *sino, int32_t B, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (B == 0) return BSCT_OK;
+  if (!c || !sino) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? forward_t<double>(p, (const double *)c, (double *)sino, B, s)
+                           : forward_t<float>(p, (const float *)c, (float *)sino, B, s);
+}
+
+bsct_status bsct_reconstruct_host(bsct_plan p, const void *sino_host, void *x_host, int32_t B, int32_t iters,
+                                  int32_t solver, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (B == 0) return BSCT_OK;
+  if (!sino_host || !x_host) return fail(BSCT_EINVAL, "NULL buffer");
+  cudaStream_t s = (cudaStream_t)stream;
+  const size_t es = p->esize();
+  const size_t sino_b = es * (size_t)p->n_angles * p->M, img_b = es * (size_t)p->N * p->N;
+  if (!p->sino_dev) CU(cudaMalloc(&p->sino_dev, sino_b * p->max_batch));
+  if (!p->b_dev) CU(cudaMalloc(&p->b_dev, img_b * p->max_batch));
+  if (!p->x_dev) CU(cudaMalloc(&p->x_dev, img_b * p->max_batch));
+  CU(cudaMemcpyAsync(p->sino_dev, sino_host, sino_b * B, cudaMemcpyHostToDevice, s));
+  st = bsct_backproject(p, p->sino_dev, p->b_dev, B, stream);
+  if (st != BSCT_OK) return st;
+  const int64_t l0 = p->launches;
+  st = bsct_cg_solve(p, p->b_dev, p->x_dev, B, iters, solver, nullptr, nullptr, stream);
+  if (st != BSCT_OK) return st;
+  p->launches += l0;
+  CU(cudaMemcpyAsync(x_host, p->x_dev, img_b * B, cudaMemcpyDeviceToHost, s));
+  CU(cudaStreamSynchronize(s));
+  return BSCT_OK;
+}
+
+int64_t bsct_plan_launch_count(bsct_plan p) { return p ? p->launches : 0; }
+
+}  // extern "C"

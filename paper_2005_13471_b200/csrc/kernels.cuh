@@ -1,0 +1,101 @@
+// kernels.cuh -- host-side launchers of the bsct kernels (internal C++ interface).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "pptable.cuh"
+
+namespace bsct {
+
+// Mutable device storage of per-angle tables (tables.cu).
+template <typename T>
+struct PPTables {
+  int *npieces = nullptr;   // [n]
+  int *nwidths = nullptr;   // [n]
+  int *degree = nullptr;    // [n]   (PP_BP: interpolation degree d)
+  double *half = nullptr;   // [n]
+  double *knots = nullptr;  // [n][PP_MAXP+1]
+  T *coef = nullptr;        // [n][PP_MAXP][PP_NC]
+  double *cs = nullptr;     // [n][2]  cos t, sin t
+  PPView<T> view() const { return PPView<T>{npieces, nwidths, half, knots, coef}; }
+  static size_t bytes(int n) {
+    return (size_t)n * (3 * sizeof(int) + sizeof(double) * (1 + (PP_MAXP + 1) + 2) + sizeof(T) * PP_MAXP * PP_NC) +
+           8 * 256;
+  }
+  // carve from one allocation
+  void carve(void *base, int n) {
+    char *p = (char *)base;
+    auto take = [&](size_t sz) { char *r = p; p += (sz + 255) & ~(size_t)255; return (void *)r; };
+    coef = (T *)take(sizeof(T) * (size_t)n * PP_MAXP * PP_NC);
+    knots = (double *)take(sizeof(double) * (size_t)n * (PP_MAXP + 1));
+    half = (double *)take(sizeof(double) * n);
+    cs = (double *)take(sizeof(double) * 2 * n);
+    npieces = (int *)take(sizeof(int) * n);
+    nwidths = (int *)take(sizeof(int) * n);
+    degree = (int *)take(sizeof(int) * n);
+  }
+};
+
+// K0 (tables.cu)
+template <typename T>
+cudaError_t build_pp_tables(const double *angles_dev, int n, int kind, double lx, double ly, double zeta,
+                            PPTables<T> out, cudaStream_t s);
+
+// K1 (gram.cu): taps[(2N-1)^2] = lx^4 sum_{a < n} M_a(lx <(-s_a, c_a), dk>)
+template <typename T>
+cudaError_t gram_taps(int N, double lx, int n, const double *cs, PPView<T> tb, T *taps, cudaStream_t s);
+
+// K2 (normal.cu): S[q][p] = Re DFT2(E)[p][q] / L^2, work >= (L/2+1)*L complex
+template <typename T>
+cudaError_t filter_spectrum(int N, int L, const T *taps, T *S, cplx<T> *work, const cplx<T> *tw, cudaStream_t s);
+
+// K5 (normal.cu): the three FFT passes of y = G x.
+//   A: x[B][N][N] -> T1[B][L/2+1][N] (row DFTs, column-major)
+//   B: T1 -> T1 (column DFT, * S, inverse column DFT, first N rows); gpart[b][blk] +=
+//      sum_q w_q S |P~|^2 partials (= <x, G x> by Parseval), may be null
+//   C: T1 -> y[B][N][N] (inverse row DFTs, first N columns)
+template <typename T>
+cudaError_t pass_a(int N, int L, int B, const T *x, cplx<T> *T1, const cplx<T> *tw, cudaStream_t s);
+template <typename T>
+cudaError_t pass_b(int N, int L, int B, cplx<T> *T1, const T *S, const cplx<T> *tw, double *gpart, cudaStream_t s);
+template <typename T>
+cudaError_t pass_c(int N, int L, int B, const cplx<T> *T1, T *y, const cplx<T> *tw, cudaStream_t s);
+int pass_b_blocks(int L);  // CTAs per slice of pass B (gpart row length)
+
+// K3/K4 (backproject.cu)
+template <typename T>
+cudaError_t correction_filter(int n_angles, int M, int B, const int *degree, const T *sino, T *gt, cudaStream_t s);
+template <typename T>
+cudaError_t backproject(int N, double lx, double ly, int n_angles, int M, int B, const double *cs, PPView<T> tb,
+                        const T *gt, T *b, cudaStream_t s);
+
+// K7 (forward.cu)
+template <typename T>
+cudaError_t forward_project(int N, double lx, double ly, int n_angles, int M, int B, const double *cs,
+                            PPView<T> tb, const T *c, T *sino, cudaStream_t s);
+
+// K6 (solver.cu)
+struct SolverWork {
+  double *rho;      // [B][iters+1]  <r_k, r_k>
+  double *alpha;    // [B]
+  double *gpart;    // [B][gstride] <d, G d> partials from pass B
+  int gstride;
+  double *rpart;    // [B][rstride] <r, r> partials
+  int rstride;
+  int *flags;       // [B] or null
+  double *resid;    // [B][iters] or null
+  double *tau;      // device scalar (Landweber)
+};
+int vec_blocks(int N);
+template <typename T>
+cudaError_t solver_init(int N, int B, const T *b, T *x, T *r, T *p, SolverWork w, int iters, cudaStream_t s);
+template <typename T>
+cudaError_t solver_update(int N, int B, int solver, int it, int iters, T *x, T *r, T *p, const T *q, SolverWork w,
+                          cudaStream_t s);
+template <typename T>
+cudaError_t solver_finish(int N, int B, int solver, int it, int iters, const T *r, T *p, SolverWork w, cudaStream_t s);
+template <typename T>
+cudaError_t spectrum_max(int L, const T *S, double *out, cudaStream_t s);
+
+}  // namespace bsct

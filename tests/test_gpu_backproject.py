@@ -1,0 +1,119 @@
+"""GPU parity, part (b): correction filter (K3, Eq.(5)) and back projection H^T g^
+(K4) vs oracle.backproject; forward projection (K7, Eq.(3)-(4)) vs
+oracle.forward; the exact-recovery property of P:140 through the CUDA path."""
+import numpy as np
+import pytest
+
+from gpu_util import geom, gpu_plan, rel_l2, to_dev, to_np, tol, uniform
+from oracle.backproject import H_CORR, backproject, corrected_row, interpolation_degree
+from oracle.forward import forward
+from synth import CONFIGS
+from synth.sinogram import config_sinogram, random_sinogram
+
+pytestmark = pytest.mark.gpu
+
+
+def gpu_bp(bsct, g, dt, sino):
+    import torch
+    B = sino.shape[0]
+    plan, taps = gpu_plan(bsct, g, dt, max_batch=B)
+    b = torch.empty((B, g["N"], g["N"]), dtype=taps.dtype, device="cuda")
+    bsct.backproject(plan, to_dev(sino, dt), b)
+    return plan, to_np(b)
+
+
+@pytest.mark.parametrize("zeta,ly,dt", [(0.0, 1.0, "f32"), (1.0, 1.0, "f64"), (1.5, 1.0, "f32"),
+                                        (0.5, 0.5, "f32"), (0.7, 1.3, "f64")])
+def test_correction_filter(cuda_lib, zeta, ly, dt):
+    import torch
+    n, M = 12, 37
+    g = geom(6, uniform(n), M, lambda_y=ly, zeta=zeta)
+    sino = random_sinogram(3, 2, n, M)
+    plan, _ = gpu_plan(cuda_lib, g, dt, max_batch=2)
+    gt = torch.empty((2, n, M + 2 * H_CORR), dtype=plan.dtype, device="cuda")
+    cuda_lib.correction_filter(plan, to_dev(sino, dt), gt)
+    got = to_np(gt)
+    for bi in range(2):
+        for a, t in enumerate(g["angles"]):
+            ref = corrected_row(sino[bi, a], interpolation_degree(g, t))
+            assert rel_l2(got[bi, a], ref) < tol(dt)
+
+
+@pytest.mark.parametrize("N,n,M,ly,zeta,dt,B", [
+    (1, 3, 5, 1.0, 0.0, "f32", 1), (4, 8, 9, 1.0, 1.0, "f64", 2), (7, 11, 15, 0.5, 0.5, "f32", 2),
+    (16, 24, 33, 1.0, 0.0, "f32", 1), (16, 24, 23, 1.3, 1.7, "f64", 1), (33, 36, 49, 1.0, 1.5, "f32", 2)])
+def test_small_full(cuda_lib, N, n, M, ly, zeta, dt, B):
+    g = geom(N, uniform(n), M, lambda_y=ly, zeta=zeta)
+    sino = random_sinogram(N + n, B, n, M)
+    _, b = gpu_bp(cuda_lib, g, dt, sino)
+    for i in range(B):
+        assert rel_l2(b[i], backproject(g, sino[i])) < tol(dt)
+
+
+def test_config1_full(cuda_lib):
+    cfg = CONFIGS[1]
+    g = cfg.geometry()
+    sino = config_sinogram(cfg)[None]
+    _, b = gpu_bp(cuda_lib, g, cfg.dtype, sino)
+    assert rel_l2(b[0], backproject(g, sino[0])) < tol(cfg.dtype)
+
+
+@pytest.mark.parametrize("ci", [2, 3, 4, 5])
+def test_config_sampled(cuda_lib, ci):
+    """Full-size back projection, 400 sampled pixels (incl. corners) checked one by one."""
+    cfg = CONFIGS[ci]
+    g = cfg.geometry()
+    sino = config_sinogram(cfg)[None]
+    _, b = gpu_bp(cuda_lib, g, cfg.dtype, sino)
+    N = cfg.N
+    rng = np.random.default_rng(ci)
+    k1 = np.concatenate([[0, 0, N - 1, N - 1, N // 2], rng.integers(0, N, 395)])
+    k2 = np.concatenate([[0, N - 1, 0, N - 1, N // 2], rng.integers(0, N, 395)])
+    ref = backproject(g, sino[0], pixels=(k1, k2))
+    assert rel_l2(b[0][k1, k2], ref) < 1e-5
+
+
+@pytest.mark.parametrize("N,n,M,ly,zeta,lx,dt", [
+    (1, 4, 7, 0.75, 0.0, 1.0, "f64"), (5, 7, 13, 0.8, 0.0, 1.0, "f32"), (6, 9, 21, 1.0, 1.0, 1.0, "f64"),
+    (9, 13, 31, 0.5, 0.4, 0.5, "f32"), (24, 30, 49, 1.0, 1.5, 1.0, "f32")])
+def test_forward(cuda_lib, N, n, M, ly, zeta, lx, dt):
+    import torch
+    g = geom(N, uniform(n) + 0.01, M, lambda_y=ly, zeta=zeta, lambda_x=lx)
+    c = np.random.default_rng(N).uniform(-1, 1, (2, N, N))
+    plan, taps = gpu_plan(cuda_lib, g, dt, max_batch=2)
+    s = torch.empty((2, n, M), dtype=taps.dtype, device="cuda")
+    cuda_lib.forward_project(plan, to_dev(c, dt), s)
+    for i in range(2):
+        assert rel_l2(to_np(s[i]), forward(g, c[i])) < tol(dt)
+
+
+def test_forward_config_sparse(cuda_lib):
+    """Config-5 geometry, sparse image (the oracle sums nonzero pixels only)."""
+    import torch
+    cfg = CONFIGS[5]
+    g = cfg.geometry()
+    N = cfg.N
+    c = np.zeros((N, N))
+    rng = np.random.default_rng(5)
+    c[rng.integers(0, N, 40), rng.integers(0, N, 40)] = rng.uniform(0, 1, 40)
+    plan, taps = gpu_plan(cuda_lib, g, "f32")
+    s = torch.empty((1, cfg.n_angles, cfg.n_det), device="cuda")
+    cuda_lib.forward_project(plan, to_dev(c[None], "f32"), s)
+    assert rel_l2(to_np(s[0]), forward(g, c)) < 1e-5
+
+
+@pytest.mark.parametrize("zeta", [0.0, 1.0])
+def test_exact_recovery_on_device(cuda_lib, zeta):
+    """BP(forward(c)) = G c at angles {0, pi/2}, lambda_y = lambda_x, all on the GPU."""
+    import torch
+    N = 20
+    g = geom(N, [0.0, np.pi / 2], 2 * N + 9, zeta=zeta)
+    plan, taps = gpu_plan(cuda_lib, g, "f64", max_batch=1)
+    c = to_dev(np.random.default_rng(4).standard_normal((1, N, N)), "f64")
+    s = torch.empty((1, 2, 2 * N + 9), dtype=torch.float64, device="cuda")
+    cuda_lib.forward_project(plan, c, s)
+    b = torch.empty_like(c)
+    cuda_lib.backproject(plan, s, b)
+    y = torch.empty_like(c)
+    cuda_lib.normal_apply(plan, c, y)
+    assert rel_l2(to_np(b), to_np(y)) < 1e-12

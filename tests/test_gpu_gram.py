@@ -1,0 +1,73 @@
+"""GPU parity, part (a): Gram filter taps (K0 tables + K1) vs oracle.gram."""
+import numpy as np
+import pytest
+
+from gpu_util import geom, gpu_taps, rel_l2, to_np, tol, uniform
+from oracle.gram import gram_taps, gram_taps_at
+from synth import CONFIGS
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("N,n,zeta,lx,dt", [
+    (1, 1, 0.0, 1.0, "f32"), (2, 3, 0.5, 1.0, "f32"), (5, 7, 0.0, 1.0, "f32"), (13, 24, 1.0, 0.7, "f32"),
+    (13, 24, 1.0, 1.0, "f64"), (33, 90, 1.5, 1.0, "f32"), (40, 36, 0.0, 1.0, "f64"), (17, 5, 2.5, 1.3, "f32")])
+def test_small_geometries(cuda_lib, N, n, zeta, lx, dt):
+    g = geom(N, uniform(n), 2 * N + 1, zeta=zeta, lambda_x=lx)
+    G = to_np(gpu_taps(cuda_lib, g, dt))
+    ref = gram_taps(g)
+    assert rel_l2(G, ref) < tol(dt)
+    assert np.abs(G - ref).max() < 10 * tol(dt) * np.abs(ref).max()
+    assert np.array_equal(G, G[::-1, ::-1])          # G[k] = G[-k] bitwise (G symmetric)
+
+
+def test_irregular_angles(cuda_lib):
+    rng = np.random.default_rng(11)
+    ang = rng.uniform(-3.0, 7.0, 29)                   # unsorted, outside [0, pi)
+    g = geom(21, ang, 45, zeta=0.8)
+    assert rel_l2(to_np(gpu_taps(cuda_lib, g, "f32")), gram_taps(g)) < 1e-5
+
+
+def test_axis_and_45deg(cuda_lib):
+    g = geom(6, [0.0, np.pi / 2, np.pi / 4], 13, zeta=0.0)
+    assert rel_l2(to_np(gpu_taps(cuda_lib, g, "f64")), gram_taps(g)) < 1e-12
+
+
+@pytest.mark.parametrize("ci", [1, 2, 3])
+def test_config_full(cuda_lib, ci):
+    cfg = CONFIGS[ci]
+    g = cfg.geometry()
+    G = to_np(gpu_taps(cuda_lib, g, cfg.dtype))
+    ref = gram_taps(g)
+    assert rel_l2(G, ref) < tol(cfg.dtype)
+
+
+def test_config4_sampled(cuda_lib):
+    """N = 1024, 720 angles, lambda_y = 0.5, zeta = 0.5 (BJ:configs[4]): every tap of the
+    central 65 x 65 block plus 4000 random taps, against the oracle tap by tap."""
+    cfg = CONFIGS[4]
+    g = cfg.geometry()
+    G = to_np(gpu_taps(cuda_lib, g, cfg.dtype))
+    N = cfg.N
+    rng = np.random.default_rng(12)
+    c = np.arange(-32, 33)
+    a = np.concatenate([np.repeat(c, c.size), rng.integers(-(N - 1), N, 4000)])
+    b = np.concatenate([np.tile(c, c.size), rng.integers(-(N - 1), N, 4000)])
+    ref = gram_taps_at(g, a, b)
+    got = G[a + N - 1, b + N - 1]
+    assert rel_l2(got, ref) < 1e-5
+
+
+def test_angle_shards_sum(cuda_lib):
+    """BJ:configs[4]: angle-sharded partial filters sum to the full filter."""
+    import torch
+    g = geom(64, uniform(90), 129, zeta=0.5, lambda_y=0.5)
+    full = gpu_taps(cuda_lib, g, "f32")
+    parts = torch.zeros_like(full)
+    tmp = torch.empty_like(full)
+    for a0, a1 in ((0, 23), (23, 45), (45, 90)):
+        cuda_lib.gram_build(g, tmp, a0, a1)
+        parts += tmp
+    assert rel_l2(to_np(parts), to_np(full)) < 1e-6
+    cuda_lib.gram_build(g, tmp, 5, 5)                # empty shard -> zeros
+    assert not tmp.any()
