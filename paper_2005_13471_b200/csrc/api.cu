@@ -1,4 +1,5 @@
 // api.cu -- the C ABI of include/bsct.h: validation, plans, launch sequencing.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -71,6 +72,10 @@ struct bsct_plan_s {
   double *angles = nullptr;
   void *bp_mem = nullptr, *fw_mem = nullptr;
   void *S = nullptr, *tw = nullptr, *spec_work = nullptr;
+  BPAngle *bp_ang = nullptr;  // K4 v2 per-angle parameters
+  void *bp_B = nullptr;       // K4 v2 basis table
+  int bp_cells = 0;           // K4 v2 tile cell capacity (0: use K4 v1)
+  bool solver_v1 = false;     // unfused 5-launch iteration (A/B testing only)
   void *T1 = nullptr, *gt = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
   void *sino_dev = nullptr, *b_dev = nullptr, *x_dev = nullptr;  // reconstruct_host staging
   double *alpha = nullptr, *gpart = nullptr, *rpart = nullptr, *tau = nullptr;
@@ -184,6 +189,9 @@ bsct_status plan_filter_t(bsct_plan p, const void *taps, cudaStream_t s) {
   PPTables<T> bp = tables_of<T>(p->bp_mem, n), fw = tables_of<T>(p->fw_mem, n);
   LAUNCH(p, BSCT_K_TABLES, 1, (build_pp_tables<T>(p->angles, n, PP_BP, p->lx, p->ly, p->zeta, bp, s)));
   LAUNCH(p, BSCT_K_TABLES, 1, (build_pp_tables<T>(p->angles, n, PP_FWD, p->lx, p->ly, p->zeta, fw, s)));
+  if (p->bp_cells > 0)
+    LAUNCH(p, BSCT_K_TABLES, 1,
+           (build_bp_tables<T>(N, p->M, p->lx, p->ly, p->zeta, n, bp, p->bp_ang, (T *)p->bp_B, s)));
   LAUNCH(p, BSCT_K_SPECTRUM, 2,
          (filter_spectrum<T>(N, L, (const T *)taps, (T *)p->S, (cplx<T> *)p->spec_work, (const cplx<T> *)p->tw, s)));
   LAUNCH(p, BSCT_K_SPECTRUM, 2, (spectrum_max<T>(L, (const T *)p->S, p->tau, s)));
@@ -206,6 +214,12 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc(&p->S, sizeof(T) * Q * L));
   CU(cudaMalloc(&p->spec_work, sizeof(cplx<T>) * Q * L));
   CU(cudaMalloc((void **)&p->tau, sizeof(double)));
+  const char *force_v1 = getenv("BSCT_BP_V1");
+  p->bp_cells = (force_v1 && force_v1[0] == '1') ? 0 : bp_v2_max_cells(p->lx, p->ly, p->zeta);
+  if (p->bp_cells > 0) {
+    CU(cudaMalloc((void **)&p->bp_ang, sizeof(BPAngle) * n));
+    CU(cudaMalloc(&p->bp_B, sizeof(T) * bp_table_floats(n)));
+  }
   bsct_status st = plan_filter_t<T>(p, taps, s);
   if (st != BSCT_OK) return st;
   // workspaces
@@ -218,7 +232,10 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc(&p->q, sizeof(T) * nn * Bz));
   CU(cudaMalloc((void **)&p->alpha, sizeof(double) * Bz));
   CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * pass_b_blocks(L)));
-  CU(cudaMalloc((void **)&p->rpart, sizeof(double) * Bz * vec_blocks(N)));
+  const size_t nrp = std::max((size_t)vec_blocks(N), (size_t)2 * fused_parts(N, L));
+  CU(cudaMalloc((void **)&p->rpart, sizeof(double) * Bz * nrp));
+  const char *sv1 = getenv("BSCT_SOLVER_V1");
+  p->solver_v1 = sv1 && sv1[0] == '1';
   CU(cudaMalloc((void **)&p->flags, sizeof(int) * Bz));
   CU(cudaStreamSynchronize(s));
   return BSCT_OK;
@@ -252,8 +269,13 @@ template <typename T>
 bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t s) {
   PPTables<T> bp = tables_of<T>(p->bp_mem, p->n_angles);
   LAUNCH(p, BSCT_K_CORRECTION, 1, (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s)));
-  LAUNCH(p, BSCT_K_BACKPROJECT, 1,
-         (backproject<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, bp.cs, bp.view(), (const T *)p->gt, b, s)));
+  if (p->bp_cells > 0)
+    LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+           (backproject_v2<T>(p->N, p->n_angles, p->M, B, p->bp_ang, (const T *)p->bp_B, (const T *)p->gt, b,
+                              p->bp_cells, p->lx * p->lx * p->ly, s)));
+  else
+    LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+           (backproject<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, bp.cs, bp.view(), (const T *)p->gt, b, s)));
   return BSCT_OK;
 }
 
@@ -266,9 +288,39 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     CU(cudaMalloc((void **)&p->rho, sizeof(double) * (size_t)(iters + 1) * (p->max_batch > 0 ? p->max_batch : 1)));
     p->rho_iters = iters;
   }
+  T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
+  if (!p->solver_v1) {
+    // fused iteration (cg.cu): 3 launches per iteration
+    FusedWork fw;
+    fw.rho = p->rho;
+    fw.rho_stride = iters + 1;
+    fw.alpha = p->alpha;
+    fw.gpart = p->gpart;
+    fw.rpart = p->rpart;
+    fw.nparts = fused_parts(p->N, p->L);
+    fw.B = B;
+    fw.flags = flags ? flags : p->flags;
+    fw.resid = resid;
+    fw.iters = iters;
+    fw.tau = p->tau;
+    auto *T1 = (cplx<T> *)p->T1;
+    auto *tw = (const cplx<T> *)p->tw;
+    const int gparts = pass_b_blocks(p->L);
+    LAUNCH(p, BSCT_K_SOLVER_INIT, 1, (fused_init<T>(p->N, B, b, x, r, solver == BSCT_CG ? pp : (T *)nullptr, fw, s)));
+    for (int it = 0; it < iters; ++it) {
+      if (solver == BSCT_CG)
+        LAUNCH(p, BSCT_K_PASS_A, 1, (fused_pass_a<T>(p->N, p->L, B, it, x, r, pp, T1, tw, fw, s)));
+      else
+        LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, B, r, T1, tw, s)));
+      LAUNCH(p, BSCT_K_PASS_B, 1,
+             (pass_b<T>(p->N, p->L, B, T1, (const T *)p->S, tw, solver == BSCT_LANDWEBER ? nullptr : p->gpart, s)));
+      LAUNCH(p, BSCT_K_PASS_C, 1, (fused_pass_c<T>(p->N, p->L, B, it, solver, gparts, T1, x, r, tw, fw, s)));
+    }
+    LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, B, iters, solver == BSCT_CG, x, pp, fw, s)));
+    return BSCT_OK;
+  }
   SolverWork w = solver_work(p, resid, flags);
   // rho rows have stride (iters + 1): the kernels index rho[b * (iters+1) + k]
-  T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
   LAUNCH(p, BSCT_K_SOLVER_INIT, 2, (solver_init<T>(p->N, B, b, x, r, solver == BSCT_CG ? pp : (T *)nullptr, w, iters, s)));
   for (int it = 0; it < iters; ++it) {
     const T *d = solver == BSCT_CG ? pp : r;
@@ -348,7 +400,7 @@ bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *
 bsct_status bsct_plan_destroy(bsct_plan p) {
   if (!p) return BSCT_OK;
   void *bufs[] = {p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->r, p->p, p->q,
-                  p->sino_dev, p->b_dev, p->x_dev, p->spec_work, p->alpha, p->gpart, p->rpart, p->tau, p->rho, p->flags};
+                  p->sino_dev, p->b_dev, p->x_dev, p->spec_work, p->bp_ang, p->bp_B, p->alpha, p->gpart, p->rpart, p->tau, p->rho, p->flags};
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : p->prof_pool) cudaEventDestroy(e);

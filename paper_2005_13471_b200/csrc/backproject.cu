@@ -120,6 +120,268 @@ cudaError_t backproject(int N, double lx, double ly, int n_angles, int M, int B,
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------------------
+// K4 v2.  With u = (k_t - y_0)/lambda_y = c + phi (cell c = floor(u), phi in [0,1)):
+//   F_t(u) = sum_m g~[m] C_t(y_m - k_t) = sum_{i} g~[c + i + imin] C_t(lambda_y (i + imin - phi)).
+// The knots of C_t map to phi-breakpoints frac((W/2 - sigma)/lambda_y) where sigma runs over
+// subset sums of the non-lambda_y widths {l|c|, l|s|, zeta} (the lambda_y widths shift knots by
+// whole cells), so the unit cell splits into P <= 9 sub-intervals on which every
+// C_t(lambda_y(i + imin - phi)) is one polynomial Q_{p,i}(tau), tau = phi - bp[p].
+// build_bp_tables: B[a][p][i][k] = coefficients of Q_{p,i} (FP64, subset sums, left half).
+// backproject_v2: per 64x64 pixel tile and angle, F[c][p][k] = sum_i g~[c+i+imin] B[p][i][k]
+// in shared memory for the tile's cells, then per pixel one sub-interval search and one
+// degree-5 Horner.  Same closed form as K4 v1 (and the oracle), different evaluation order.
+// ----------------------------------------------------------------------------------------
+
+size_t bp_table_floats(int n) { return (size_t)n * BP_PMAX * BP_SMAX * 8; }
+
+template <typename T>
+__global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx, double ly, double zeta, int n,
+                                                        const double *__restrict__ cs, const int *__restrict__ degree,
+                                                        BPAngle *__restrict__ ang, T *__restrict__ Btab) {
+  const int a = blockIdx.x;
+  const int tid = threadIdx.x;
+  __shared__ double w[8], sig[64], bp[16], wb[4];
+  __shared__ int sgn[64], nw, nbase, P, S, imin;
+  __shared__ double H;
+  if (a >= n) return;
+  const double c = cs[2 * a], s = cs[2 * a + 1];
+  if (tid == 0) {
+    double raw[8];
+    int nr = 0;
+    raw[nr++] = lx * fabs(c);
+    raw[nr++] = lx * fabs(s);
+    if (zeta > 0) raw[nr++] = zeta;
+    const int d = degree[a];
+    const int nbr = nr;
+    for (int i = 0; i <= d; ++i) raw[nr++] = ly;
+    double ssum = 0;
+    for (int i = 0; i < nr; ++i) ssum += raw[i];
+    const double thr = 1e-12 * fmax(1.0, ssum);
+    int k = 0, kb = 0;
+    for (int i = 0; i < nr; ++i)
+      if (raw[i] > thr) {
+        w[k++] = raw[i];
+        if (i < nbr) wb[kb++] = raw[i];
+      }
+    nw = k;
+    nbase = kb;
+    double W = 0;
+    for (int i = 0; i < k; ++i) W += w[i];
+    H = 0.5 * W;
+    const int cw = (int)ceil(H / ly - 1e-12);
+    imin = -cw;
+    S = 2 * cw + 1;
+    // phi breakpoints
+    double f[9];
+    int nf = 0;
+    f[nf++] = 0.0;
+    for (int m = 0; m < (1 << kb); ++m) {
+      double sg = 0;
+      for (int i = 0; i < kb; ++i)
+        if ((m >> i) & 1) sg += wb[i];
+      double v = (H - sg) / ly;
+      v -= floor(v);
+      if (v > 1.0 - 1e-12) v = 0.0;
+      f[nf++] = v;
+    }
+    for (int i = 1; i < nf; ++i)  // insertion sort
+      for (int j = i; j > 0 && f[j] < f[j - 1]; --j) { double t = f[j]; f[j] = f[j - 1]; f[j - 1] = t; }
+    int np = 0;
+    for (int i = 0; i < nf; ++i)
+      if (np == 0 || f[i] > bp[np - 1] + 1e-12) bp[np++] = f[i];
+    P = np;
+    BPAngle A;
+    const double x0 = lx * (double)(0 - N / 2), y0 = ly * (double)(0 - M / 2);
+    A.u0 = (fma(-s, x0, c * x0) - y0) / ly;
+    A.du1 = -s * lx / ly;
+    A.du2 = c * lx / ly;
+    for (int i = 0; i < BP_PMAX; ++i) A.bp[i] = i < np ? bp[i] : 3.0e38;
+    A.P = np;
+    A.S = S;
+    A.imin = -cw;
+    A.pad = 0;
+    ang[a] = A;
+  }
+  __syncthreads();
+  const int n_w = nw, ns = 1 << n_w;
+  if (tid < ns) {
+    double sm = 0;
+    int pc = 0;
+    for (int i = 0; i < n_w; ++i)
+      if ((tid >> i) & 1) { sm += w[i]; ++pc; }
+    sig[tid] = sm;
+    sgn[tid] = (pc & 1) ? -1 : 1;
+  }
+  __syncthreads();
+  double prodw = 1.0, fact = 1.0;
+  for (int i = 0; i < n_w; ++i) prodw *= w[i];
+  for (int i = 2; i < n_w; ++i) fact *= i;
+  const double norm = 1.0 / (fact * prodw);
+  const int deg = n_w - 1;
+  const double Hh = H;
+  T *Ba = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
+  for (int item = tid; item < BP_PMAX * BP_SMAX; item += blockDim.x) {
+    const int p = item / BP_SMAX, i = item % BP_SMAX;
+    double coef[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (p < P && i < S) {
+      const double ph = bp[p], phn = (p + 1 < P) ? bp[p + 1] : 1.0;
+      const double x0 = ly * ((double)(i + imin) - ph);  // argument at tau = 0; x(tau) = x0 - ly tau
+      const double e = x0 - 0.5 * ly * (phn - ph);        // interior point of the range
+      if (fabs(e) < Hh) {
+        // even symmetry: evaluate on the left half, y(tau) = y0 + g tau
+        const bool fl = e > 0;
+        const double y0v = fl ? -x0 : x0, g = fl ? ly : -ly, ye = fl ? -e : e;
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        for (int S2 = 0; S2 < ns; ++S2) {
+          if (!(sig[S2] - Hh < ye)) continue;  // knot right of the range: inactive
+          const double dl = fmax(0.0, y0v + Hh - sig[S2]);
+          double pw = 1.0;  // dl^(deg-k) for k = deg..0
+          for (int k = deg; k >= 0; --k) {
+            acc[k] += sgn[S2] * pw;
+            pw *= dl;
+          }
+        }
+        double binom = 1.0, gk = 1.0;
+        for (int k = 0; k <= deg; ++k) {
+          coef[k] = norm * binom * gk * acc[k];
+          binom = binom * (deg - k) / (k + 1);
+          gk *= g;
+        }
+      }
+    }
+    for (int k = 0; k < 8; ++k) Ba[(size_t)item * 8 + k] = (T)coef[k];
+  }
+}
+
+template <typename T>
+cudaError_t build_bp_tables(int N, int M, double lx, double ly, double zeta, int n, const PPTables<T> &tb,
+                            BPAngle *ang, T *Btab, cudaStream_t s) {
+  bp_tables_kernel<T><<<n, 128, 0, s>>>(N, M, lx, ly, zeta, n, tb.cs, tb.degree, ang, Btab);
+  return cudaGetLastError();
+}
+
+constexpr int BPT = 64;          // tile edge (pixels)
+constexpr int BP_ROWS = 16;      // rows per thread
+constexpr int BP_THREADS = 256;  // 8 warps = 4 (rows of 16) x 2 (32 columns)
+
+template <typename T>
+__device__ __forceinline__ T horner6(const T *e, T t) {
+  T r = e[5];
+  r = fma(r, t, e[4]);
+  r = fma(r, t, e[3]);
+  r = fma(r, t, e[2]);
+  r = fma(r, t, e[1]);
+  r = fma(r, t, e[0]);
+  return r;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(BP_THREADS) bp_v2_kernel(int N, int n_angles, int M, const BPAngle *__restrict__ ang,
+                                                           const T *__restrict__ Btab, const T *__restrict__ gt,
+                                                           T *__restrict__ out, int max_cells, T scale) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T *tab = reinterpret_cast<T *>(smem_raw);                       // [2][max_cells * (BP_PMAX/.. stride)]
+  __shared__ T sbp[2][BP_PMAX];
+  const int tstride = max_cells * (9 * 8 + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tk1 = blockIdx.y * BPT, tk2 = blockIdx.x * BPT;
+  const int k1_0 = tk1 + (warp >> 1) * BP_ROWS;
+  const int k2 = tk2 + (warp & 1) * 32 + lane;
+  const int b = blockIdx.z;
+  const int Mt = M + 2 * HC;
+  const T *g = gt + (size_t)b * n_angles * Mt;
+  T acc[BP_ROWS];
+#pragma unroll
+  for (int j = 0; j < BP_ROWS; ++j) acc[j] = 0;
+  for (int a = 0; a < n_angles; ++a) {
+    const BPAngle &A = ang[a];
+    const double u0 = A.u0, du1 = A.du1, du2 = A.du2;
+    const int P = A.P, S = A.S, imin = A.imin;
+    // tile cell range from its corners
+    const double ua = fma(du1, (double)tk1, fma(du2, (double)tk2, u0));
+    const double e1 = du1 * (BPT - 1), e2 = du2 * (BPT - 1);
+    const double umin = ua + fmin(0.0, e1) + fmin(0.0, e2), umax = ua + fmax(0.0, e1) + fmax(0.0, e2);
+    const int c_lo = (int)floor(umin) - 1;
+    const int ncell = min((int)floor(umax) - c_lo + 2, max_cells);
+    const int stride = P * 8 + 4;
+    T *buf = tab + (a & 1) * tstride;
+    if (threadIdx.x < BP_PMAX) sbp[a & 1][threadIdx.x] = (T)A.bp[threadIdx.x];
+    const T *Ba = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
+    const T *ga = g + (size_t)a * Mt + HC;  // ga[m] = g~ at detector index m (m in [-HC, M+HC))
+    for (int item = threadIdx.x; item < P * ncell; item += BP_THREADS) {
+      const int p = item / ncell, cc = item - p * ncell;
+      const int c0 = c_lo + cc + imin;
+      T f[6] = {0, 0, 0, 0, 0, 0};
+      const T *Bp = Ba + (size_t)p * BP_SMAX * 8;
+      for (int i = 0; i < S; ++i) {
+        const int m = c0 + i;
+        if (m < -HC || m >= M + HC) continue;
+        const T gv = ga[m];
+        const T *Bi = Bp + i * 8;
+#pragma unroll
+        for (int k = 0; k < 6; ++k) f[k] = fma(gv, Bi[k], f[k]);
+      }
+      T *e = buf + cc * stride + p * 8;
+#pragma unroll
+      for (int k = 0; k < 6; ++k) e[k] = f[k];
+    }
+    __syncthreads();
+    const T *bpv = sbp[a & 1];
+    const double ub = fma(du1, (double)k1_0, fma(du2, (double)k2, u0));
+    const double cb = floor(ub);
+    const T fb = (T)(ub - cb);
+    const int cbi = (int)cb - c_lo;
+    const T d1 = (T)du1;
+#pragma unroll
+    for (int j = 0; j < BP_ROWS; ++j) {
+      const T v = fma(d1, (T)j, fb);
+      const T cf = floor(v);
+      const T ph = v - cf;
+      const int cc = cbi + (int)cf;
+      int p = 0;
+      if (bpv[p + 8] <= ph) p += 8;
+      if (bpv[p + 4] <= ph) p += 4;
+      if (bpv[p + 2] <= ph) p += 2;
+      if (bpv[p + 1] <= ph) p += 1;
+      const T tau = (T)(ph - bpv[p]);
+      acc[j] += horner6<T>(buf + cc * stride + p * 8, tau);
+    }
+  }
+  if (k2 < N) {
+    T *o = out + (size_t)b * N * N;
+#pragma unroll
+    for (int j = 0; j < BP_ROWS; ++j)
+      if (k1_0 + j < N) o[(size_t)(k1_0 + j) * N + k2] = scale * acc[j];
+  }
+}
+
+template <typename T>
+cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
+                           int max_cells, double scale, cudaStream_t s) {
+  const size_t sm = sizeof(T) * 2 * (size_t)max_cells * (9 * 8 + 4);
+  cudaError_t e = cudaFuncSetAttribute(bp_v2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid((N + BPT - 1) / BPT, (N + BPT - 1) / BPT, B);
+  bp_v2_kernel<T><<<grid, BP_THREADS, sm, s>>>(N, n_angles, M, ang, Btab, gt, b, max_cells, (T)scale);
+  return cudaGetLastError();
+}
+
+int bp_v2_max_cells(double lx, double ly, double zeta) {
+  const double H = 0.5 * (lx * 1.4142135623730951 + zeta + 3.0 * ly);
+  const int S = 2 * (int)ceil(H / ly) + 1;
+  if (S > BP_SMAX) return 0;  // too many samples per cell: use K4 v1
+  return (int)ceil((BPT - 1) * lx * 1.4142135623730951 / ly) + 5;
+}
+
+template cudaError_t build_bp_tables<float>(int, int, double, double, double, int, const PPTables<float> &, BPAngle *,
+                                            float *, cudaStream_t);
+template cudaError_t build_bp_tables<double>(int, int, double, double, double, int, const PPTables<double> &,
+                                             BPAngle *, double *, cudaStream_t);
+template cudaError_t backproject_v2<float>(int, int, int, int, const BPAngle *, const float *, const float *, float *,
+                                           int, double, cudaStream_t);
+template cudaError_t backproject_v2<double>(int, int, int, int, const BPAngle *, const double *, const double *,
+                                            double *, int, double, cudaStream_t);
 template cudaError_t correction_filter<float>(int, int, int, const int *, const float *, float *, cudaStream_t);
 template cudaError_t correction_filter<double>(int, int, int, const int *, const double *, double *, cudaStream_t);
 template cudaError_t backproject<float>(int, double, double, int, int, int, const double *, PPView<float>,

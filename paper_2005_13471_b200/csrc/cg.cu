@@ -1,0 +1,355 @@
+// cg.cu -- K5+K6 fused solver iteration: three launches per iteration (north_star "CG loop",
+// P:34 "apply the filter in every iteration", P:210 steepest descent).
+//
+// CG (textbook recurrences, FP64 per-slice scalars):
+//   pass A(k):  rho_k = <r_k, r_k> (reduced from pass C(k-1) partials), beta = rho_k / rho_{k-1},
+//               x_k = x_{k-1} + alpha_{k-1} p_{k-1},  p_k = r_k + beta p_{k-1},  row DFTs of pad(p_k)
+//   pass B(k):  column DFT, * spectrum, inverse column DFT; gamma_k = <p_k, G p_k> by Parseval
+//   pass C(k):  alpha_k = rho_k / gamma_k; inverse row DFTs -> (G p_k) rows;
+//               r_{k+1} = r_k - alpha_k G p_k; partials of <r_{k+1}, r_{k+1}>
+//   final:      x_K = x_{K-1} + alpha_{K-1} p_{K-1}; rho_K
+// G p_k never touches HBM.  Steepest descent / Landweber use pass A of normal.cu on r and
+// update x in pass C (x += alpha r_k before r is overwritten).
+// Partials of <r,r> are double-buffered by iteration parity so that a kernel may read the
+// previous partials while writing the next ones.
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace bsct {
+
+__device__ __forceinline__ double cta_sum(double v, double *red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double s = 0;
+  const int nw = (blockDim.x + 31) >> 5;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+__device__ __forceinline__ double cta_reduce_parts(const double *__restrict__ parts, int n, double *red) {
+  double v = 0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) v += parts[i];
+  return cta_sum(v, red);
+}
+
+// ---------------------------------------------------------------- init: x = 0, r = p = b, partials of <b,b>
+template <typename T>
+__global__ void __launch_bounds__(256) cg_init_kernel(long n, const T *__restrict__ b, T *__restrict__ x,
+                                                      T *__restrict__ r, T *__restrict__ p, FusedWork w) {
+  __shared__ double red[32];
+  const size_t off = (size_t)blockIdx.y * n;
+  double acc = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const T v = b[off + i];
+    x[off + i] = 0;
+    r[off + i] = v;
+    if (p) p[off + i] = v;
+    acc += (double)v * v;
+  }
+  const double s = cta_sum(acc, red);
+  if (threadIdx.x == 0) w.rpart[(size_t)blockIdx.y * w.nparts + blockIdx.x] = s;  // parity 0
+  if (blockIdx.x == 0 && threadIdx.x == 0 && w.flags) w.flags[blockIdx.y] = 0;
+}
+
+// ---------------------------------------------------------------- pass A (CG): p-update fused with row DFTs
+template <typename T, int L>
+__global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N, int k, T *__restrict__ x,
+                                                                          const T *__restrict__ r,
+                                                                          T *__restrict__ p,
+                                                                          cplx<T> *__restrict__ T1,
+                                                                          const cplx<T> *__restrict__ tw,
+                                                                          FusedWork w) {
+  using Cf = FftCfg<L>;
+  using V = cplx<T>;
+  constexpr int G = FftLaunch<L>::G, P = Cf::P, E = Cf::E, Q = L / 2 + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V *smem = reinterpret_cast<V *>(smem_raw);
+  __shared__ double red[32];
+  const int g = threadIdx.x / P, t = threadIdx.x % P;
+  const int b = blockIdx.y;
+  // scalars of slice b
+  const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+  double beta = 0.0, alpha_prev = 0.0;
+  if (k > 0) {
+    const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
+    beta = rho_prev > 0 ? rho / rho_prev : 0.0;
+    alpha_prev = w.alpha[b];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w.rho[(size_t)b * w.rho_stride + k] = rho;
+    if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+  }
+  const T be = (T)beta, al = (T)alpha_prev;
+  const int row0 = blockIdx.x * 2 * G;
+  const int ra = row0 + 2 * g, rb = ra + 1;
+  const size_t so = (size_t)b * N * N;
+  V v[E];
+#pragma unroll
+  for (int rr = 0; rr < E; ++rr) {
+    const int j = t + rr * P;
+    T va = 0, vb = 0;
+    if (j < N) {
+      if (ra < N) {
+        const size_t i = so + (size_t)ra * N + j;
+        const T po = p[i];
+        x[i] = fma(al, po, x[i]);
+        va = fma(be, po, r[i]);
+        p[i] = va;
+      }
+      if (rb < N) {
+        const size_t i = so + (size_t)rb * N + j;
+        const T po = p[i];
+        x[i] = fma(al, po, x[i]);
+        vb = fma(be, po, r[i]);
+        p[i] = vb;
+      }
+    }
+    v[rr] = V{va, vb};
+  }
+  V *sm = smem + g * Cf::SMEM;
+  fft_group<T, L, false>(v, sm, tw, t);
+  V *T1s = T1 + (size_t)b * Q * N;
+  for (int idx = threadIdx.x; idx < Q * G; idx += blockDim.x) {
+    const int q = idx / G, gg = idx % G;
+    const int ra2 = row0 + 2 * gg;
+    if (ra2 >= N) continue;
+    const V *s2 = smem + gg * Cf::SMEM;
+    const V z = s2[pidx(q)];
+    const V zc = s2[pidx((L - q) & (L - 1))];
+    T1s[(size_t)q * N + ra2] = V{(T)0.5 * (z.x + zc.x), (T)0.5 * (z.y - zc.y)};
+    if (ra2 + 1 < N) T1s[(size_t)q * N + ra2 + 1] = V{(T)0.5 * (z.y + zc.y), (T)0.5 * (zc.x - z.x)};
+  }
+}
+
+// ---------------------------------------------------------------- pass C: inverse row DFTs fused with the r update
+// MODE 0: CG (x deferred to pass A); 1: steepest descent; 2: Landweber (alpha = tau)
+template <typename T, int L, int MODE>
+__global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_c_kernel(int N, int k, int gparts,
+                                                                          const cplx<T> *__restrict__ T1,
+                                                                          T *__restrict__ x, T *__restrict__ r,
+                                                                          const cplx<T> *__restrict__ tw,
+                                                                          FusedWork w) {
+  using Cf = FftCfg<L>;
+  using V = cplx<T>;
+  constexpr int G = FftLaunch<L>::G, P = Cf::P, E = Cf::E, Q = L / 2 + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V *smem = reinterpret_cast<V *>(smem_raw);
+  __shared__ double red[32];
+  const int g = threadIdx.x / P, t = threadIdx.x % P;
+  const int b = blockIdx.y;
+  double rho;
+  if (MODE == 0) {
+    rho = w.rho[(size_t)b * w.rho_stride + k];
+  } else {
+    rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+  }
+  double alpha;
+  if (MODE == 2) {
+    alpha = *w.tau;
+  } else {
+    const double gam = cta_reduce_parts(w.gpart + (size_t)b * gparts, gparts, red);
+    const bool bad = rho > 0 && !(gam > 0);
+    const bool frozen = bad || (w.flags && w.flags[b]);
+    alpha = (rho > 0 && !frozen) ? rho / gam : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
+  const T al = (T)alpha;
+  const int row0 = blockIdx.x * 2 * G;
+  const V *T1s = T1 + (size_t)b * Q * N;
+  for (int idx = threadIdx.x; idx < Q * G; idx += blockDim.x) {
+    const int q = idx / G, gg = idx % G;
+    const int ra2 = row0 + 2 * gg;
+    V xa = V{0, 0}, xb = V{0, 0};
+    if (ra2 < N) {
+      xa = T1s[(size_t)q * N + ra2];
+      if (ra2 + 1 < N) xb = T1s[(size_t)q * N + ra2 + 1];
+    }
+    if (q == 0 || q == L / 2) { xa.y = 0; xb.y = 0; }
+    V *s2 = smem + gg * Cf::SMEM;
+    s2[pidx(q)] = V{xa.x - xb.y, xa.y + xb.x};
+    if (q != 0 && q != L / 2) s2[pidx(L - q)] = V{xa.x + xb.y, xb.x - xa.y};
+  }
+  __syncthreads();
+  V *sm = smem + g * Cf::SMEM;
+  V v[E];
+#pragma unroll
+  for (int rr = 0; rr < E; ++rr) v[rr] = sm[pidx(t + rr * P)];
+  __syncthreads();
+  fft_group<T, L, true>(v, sm, tw, t);
+  const int ra = row0 + 2 * g, rb = ra + 1;
+  const size_t so = (size_t)b * N * N;
+  double acc = 0;
+#pragma unroll
+  for (int rr = 0; rr < E; ++rr) {
+    const int n = t + rr * P;
+    if (n < N) {
+      const V z = sm[pidx(n)];
+      if (ra < N) {
+        const size_t i = so + (size_t)ra * N + n;
+        const T ro = r[i];
+        if (MODE != 0) x[i] = fma(al, ro, x[i]);
+        const T rn = fma(-al, z.x, ro);
+        r[i] = rn;
+        acc += (double)rn * rn;
+      }
+      if (rb < N) {
+        const size_t i = so + (size_t)rb * N + n;
+        const T ro = r[i];
+        if (MODE != 0) x[i] = fma(al, ro, x[i]);
+        const T rn = fma(-al, z.y, ro);
+        r[i] = rn;
+        acc += (double)rn * rn;
+      }
+    }
+  }
+  const double s = cta_sum(acc, red);
+  if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
+}
+
+// ---------------------------------------------------------------- final: rho_K, resid, CG x update
+template <typename T>
+__global__ void __launch_bounds__(256) cg_final_kernel(long n, int K, int cg, T *__restrict__ x,
+                                                       const T *__restrict__ p, FusedWork w) {
+  __shared__ double red[32];
+  const int b = blockIdx.y;
+  const double rho = cta_reduce_parts(w.rpart + ((size_t)(K & 1) * w.B + b) * w.nparts, w.nparts, red);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w.rho[(size_t)b * w.rho_stride + K] = rho;
+    if (K > 0 && w.resid) w.resid[(size_t)b * w.iters + K - 1] = sqrt(rho);
+  }
+  if (!cg || K == 0) return;
+  const T al = (T)w.alpha[b];
+  const size_t off = (size_t)b * n;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    x[off + i] = fma(al, p[off + i], x[off + i]);
+}
+
+// ---------------------------------------------------------------- launchers
+template <int L>
+static int fused_parts_L(int N) {
+  constexpr int G = FftLaunch<L>::G;
+  return (N + 2 * G - 1) / (2 * G);
+}
+
+int fused_parts(int N, int L) {
+  switch (L) {
+    case 2: return fused_parts_L<2>(N);
+    case 4: return fused_parts_L<4>(N);
+    case 8: return fused_parts_L<8>(N);
+    case 16: return fused_parts_L<16>(N);
+    case 32: return fused_parts_L<32>(N);
+    case 64: return fused_parts_L<64>(N);
+    case 128: return fused_parts_L<128>(N);
+    case 256: return fused_parts_L<256>(N);
+    case 512: return fused_parts_L<512>(N);
+    case 1024: return fused_parts_L<1024>(N);
+    case 2048: return fused_parts_L<2048>(N);
+    case 4096: return fused_parts_L<4096>(N);
+  }
+  return 0;
+}
+
+template <int L>
+constexpr size_t cg_smem(size_t elem) { return (size_t)FftLaunch<L>::G * FftCfg<L>::SMEM * elem; }
+
+template <typename K>
+static cudaError_t cg_set_smem(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return cudaSuccess;
+}
+
+template <typename T, int L>
+static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
+                               FusedWork w, cudaStream_t s) {
+  const size_t sm = cg_smem<L>(sizeof(cplx<T>));
+  cudaError_t e = cg_set_smem(cg_pass_a_kernel<T, L>, sm);
+  if (e != cudaSuccess) return e;
+  cg_pass_a_kernel<T, L><<<dim3(w.nparts, B), FftLaunch<L>::THREADS, sm, s>>>(N, k, x, r, p, T1, tw, w);
+  return cudaGetLastError();
+}
+
+template <typename T, int L>
+static cudaError_t cg_pass_c_L(int N, int B, int k, int mode, int gparts, const cplx<T> *T1, T *x, T *r,
+                               const cplx<T> *tw, FusedWork w, cudaStream_t s) {
+  const size_t sm = cg_smem<L>(sizeof(cplx<T>));
+  const dim3 grid(w.nparts, B);
+  cudaError_t e;
+  switch (mode) {
+    case 0:
+      e = cg_set_smem(cg_pass_c_kernel<T, L, 0>, sm);
+      if (e != cudaSuccess) return e;
+      cg_pass_c_kernel<T, L, 0><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r, tw, w);
+      break;
+    case 1:
+      e = cg_set_smem(cg_pass_c_kernel<T, L, 1>, sm);
+      if (e != cudaSuccess) return e;
+      cg_pass_c_kernel<T, L, 1><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r, tw, w);
+      break;
+    default:
+      e = cg_set_smem(cg_pass_c_kernel<T, L, 2>, sm);
+      if (e != cudaSuccess) return e;
+      cg_pass_c_kernel<T, L, 2><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r, tw, w);
+  }
+  return cudaGetLastError();
+}
+
+#define CG_L_SWITCH(L, CALL)                             \
+  switch (L) {                                           \
+    case 2: { constexpr int LL = 2; CALL; } break;       \
+    case 4: { constexpr int LL = 4; CALL; } break;       \
+    case 8: { constexpr int LL = 8; CALL; } break;       \
+    case 16: { constexpr int LL = 16; CALL; } break;     \
+    case 32: { constexpr int LL = 32; CALL; } break;     \
+    case 64: { constexpr int LL = 64; CALL; } break;     \
+    case 128: { constexpr int LL = 128; CALL; } break;   \
+    case 256: { constexpr int LL = 256; CALL; } break;   \
+    case 512: { constexpr int LL = 512; CALL; } break;   \
+    case 1024: { constexpr int LL = 1024; CALL; } break; \
+    case 2048: { constexpr int LL = 2048; CALL; } break; \
+    case 4096: { constexpr int LL = 4096; CALL; } break; \
+    default: return cudaErrorInvalidValue;               \
+  }
+
+template <typename T>
+cudaError_t fused_init(int N, int B, const T *b, T *x, T *r, T *p, FusedWork w, cudaStream_t s) {
+  cg_init_kernel<T><<<dim3(w.nparts, B), 256, 0, s>>>((long)N * N, b, x, r, p, w);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t fused_pass_a(int N, int L, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
+                         FusedWork w, cudaStream_t s) {
+  CG_L_SWITCH(L, return (cg_pass_a_L<T, LL>(N, B, k, x, r, p, T1, tw, w, s)));
+}
+template <typename T>
+cudaError_t fused_pass_c(int N, int L, int B, int k, int mode, int gparts, const cplx<T> *T1, T *x, T *r,
+                         const cplx<T> *tw, FusedWork w, cudaStream_t s) {
+  CG_L_SWITCH(L, return (cg_pass_c_L<T, LL>(N, B, k, mode, gparts, T1, x, r, tw, w, s)));
+}
+template <typename T>
+cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork w, cudaStream_t s) {
+  const long n = (long)N * N;
+  int vb = (int)((n + 2047) / 2048);
+  vb = vb < 1 ? 1 : (vb > 128 ? 128 : vb);
+  cg_final_kernel<T><<<dim3(cg ? vb : 1, B), 256, 0, s>>>(n, K, cg, x, p, w);
+  return cudaGetLastError();
+}
+
+#define CG_INST(T)                                                                                               \
+  template cudaError_t fused_init<T>(int, int, const T *, T *, T *, T *, FusedWork, cudaStream_t);               \
+  template cudaError_t fused_pass_a<T>(int, int, int, int, T *, const T *, T *, cplx<T> *, const cplx<T> *,     \
+                                       FusedWork, cudaStream_t);                                               \
+  template cudaError_t fused_pass_c<T>(int, int, int, int, int, int, const cplx<T> *, T *, T *, const cplx<T> *, \
+                                       FusedWork, cudaStream_t);                                               \
+  template cudaError_t fused_final<T>(int, int, int, int, T *, const T *, FusedWork, cudaStream_t);
+CG_INST(float)
+CG_INST(double)
+
+}  // namespace bsct

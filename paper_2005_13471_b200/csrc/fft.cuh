@@ -183,4 +183,13 @@ struct FftLaunch {
   static constexpr int THREADS = G * P;
 };
 
+// Pass B (two FFTs per column, the heaviest register user) uses fewer columns per CTA so
+// that several CTAs share an SM and hide each other's barrier stalls.
+template <int L>
+struct FftLaunchB {
+  static constexpr int P = FftCfg<L>::P;
+  static constexpr int G = L >= 512 ? 2 : FftLaunch<L>::G;
+  static constexpr int THREADS = G * P;
+};
+
 }  // namespace bsct

@@ -70,6 +70,25 @@ template <typename T>
 cudaError_t backproject(int N, double lx, double ly, int n_angles, int M, int B, const double *cs, PPView<T> tb,
                         const T *gt, T *b, cudaStream_t s);
 
+// K4 v2: per-angle sub-interval basis (bp_tables) + per-tile piecewise polynomial of
+// F_t(u) = sum_m g~[m] C_t(y_m - k_t) in shared memory (backproject.cu).
+constexpr int BP_PMAX = 16;   // sub-intervals of the unit detector cell (<= 9 used: 8 subset sums + wrap)
+constexpr int BP_SMAX = 12;   // detector samples touching one cell's pixels
+struct BPAngle {
+  double u0;        // (k_t(pixel 0,0) - y_0) / lambda_y
+  double du1, du2;  // d u / d k1, d u / d k2
+  double bp[BP_PMAX];  // sub-interval starts in [0,1), bp[0] = 0, unused = +huge
+  int P, S, imin, pad;
+};
+size_t bp_table_floats(int n);  // size of the basis table B[n][BP_PMAX][BP_SMAX][8]
+int bp_v2_max_cells(double lx, double ly, double zeta);  // 0: geometry not supported by v2
+template <typename T>
+cudaError_t build_bp_tables(int N, int M, double lx, double ly, double zeta, int n, const PPTables<T> &tb,
+                            BPAngle *ang, T *Btab, cudaStream_t s);
+template <typename T>
+cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
+                           int max_cells, double scale, cudaStream_t s);
+
 // K7 (forward.cu)
 template <typename T>
 cudaError_t forward_project(int N, double lx, double ly, int n_angles, int M, int B, const double *cs,
@@ -88,6 +107,32 @@ struct SolverWork {
   double *tau;      // device scalar (Landweber)
 };
 int vec_blocks(int N);
+
+// fused solver iteration (cg.cu): pass A(CG) / pass C with the vector updates folded in
+struct FusedWork {
+  double *rho;     // [B][rho_stride]
+  int rho_stride;
+  double *alpha;   // [B]
+  double *gpart;   // [B][gparts] from pass B
+  double *rpart;   // [2][B][nparts] <r,r> partials, by iteration parity
+  int nparts;      // pass A / pass C CTAs per slice
+  int B;
+  int *flags;      // [B] or null
+  double *resid;   // [B][iters] or null
+  int iters;
+  double *tau;     // Landweber step (device)
+};
+int fused_parts(int N, int L);
+template <typename T>
+cudaError_t fused_init(int N, int B, const T *b, T *x, T *r, T *p, FusedWork w, cudaStream_t s);
+template <typename T>
+cudaError_t fused_pass_a(int N, int L, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
+                         FusedWork w, cudaStream_t s);
+template <typename T>
+cudaError_t fused_pass_c(int N, int L, int B, int k, int mode, int gparts, const cplx<T> *T1, T *x, T *r,
+                         const cplx<T> *tw, FusedWork w, cudaStream_t s);
+template <typename T>
+cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork w, cudaStream_t s);
 template <typename T>
 cudaError_t solver_init(int N, int B, const T *b, T *x, T *r, T *p, SolverWork w, int iters, cudaStream_t s);
 template <typename T>

@@ -60,13 +60,13 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) pass_a_kernel(int N, co
 
 // ---------------------------------------------------------------- pass B
 template <typename T, int L>
-__global__ void __launch_bounds__(FftLaunch<L>::THREADS) pass_b_kernel(int N, cplx<T> *__restrict__ T1,
+__global__ void __launch_bounds__(FftLaunchB<L>::THREADS) pass_b_kernel(int N, cplx<T> *__restrict__ T1,
                                                                        const T *__restrict__ S,
                                                                        const cplx<T> *__restrict__ tw,
                                                                        double *__restrict__ gpart) {
   using Cf = FftCfg<L>;
   using V = cplx<T>;
-  constexpr int G = FftLaunch<L>::G, P = Cf::P, E = Cf::E, Q = L / 2 + 1;
+  constexpr int G = FftLaunchB<L>::G, P = Cf::P, E = Cf::E, Q = L / 2 + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V *smem = reinterpret_cast<V *>(smem_raw);
   __shared__ double red[32];
@@ -276,12 +276,12 @@ static cudaError_t pass_a_L(int N, int B, const T *x, cplx<T> *T1, const cplx<T>
 }
 template <typename T, int L>
 static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T> *tw, double *gpart, cudaStream_t s) {
-  constexpr int G = FftLaunch<L>::G;
-  const size_t sm = fft_smem_bytes<L>(sizeof(cplx<T>));
+  constexpr int G = FftLaunchB<L>::G;
+  const size_t sm = (size_t)G * FftCfg<L>::SMEM * sizeof(cplx<T>);
   cudaError_t e = set_smem(pass_b_kernel<T, L>, sm);
   if (e != cudaSuccess) return e;
   dim3 grid((L / 2 + 1 + G - 1) / G, B);
-  pass_b_kernel<T, L><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, T1, S, tw, gpart);
+  pass_b_kernel<T, L><<<grid, FftLaunchB<L>::THREADS, sm, s>>>(N, T1, S, tw, gpart);
   return cudaGetLastError();
 }
 template <typename T, int L>
@@ -309,18 +309,18 @@ static cudaError_t spectrum_L(int N, const T *taps, T *S, cplx<T> *work, const c
 
 int pass_b_blocks(int L) {
   switch (L) {
-    case 2: return (2 / 2 + 1 + FftLaunch<2>::G - 1) / FftLaunch<2>::G;
-    case 4: return (4 / 2 + 1 + FftLaunch<4>::G - 1) / FftLaunch<4>::G;
-    case 8: return (8 / 2 + 1 + FftLaunch<8>::G - 1) / FftLaunch<8>::G;
-    case 16: return (16 / 2 + 1 + FftLaunch<16>::G - 1) / FftLaunch<16>::G;
-    case 32: return (32 / 2 + 1 + FftLaunch<32>::G - 1) / FftLaunch<32>::G;
-    case 64: return (64 / 2 + 1 + FftLaunch<64>::G - 1) / FftLaunch<64>::G;
-    case 128: return (128 / 2 + 1 + FftLaunch<128>::G - 1) / FftLaunch<128>::G;
-    case 256: return (256 / 2 + 1 + FftLaunch<256>::G - 1) / FftLaunch<256>::G;
-    case 512: return (512 / 2 + 1 + FftLaunch<512>::G - 1) / FftLaunch<512>::G;
-    case 1024: return (1024 / 2 + 1 + FftLaunch<1024>::G - 1) / FftLaunch<1024>::G;
-    case 2048: return (2048 / 2 + 1 + FftLaunch<2048>::G - 1) / FftLaunch<2048>::G;
-    case 4096: return (4096 / 2 + 1 + FftLaunch<4096>::G - 1) / FftLaunch<4096>::G;
+    case 2: return (2 / 2 + 1 + FftLaunchB<2>::G - 1) / FftLaunchB<2>::G;
+    case 4: return (4 / 2 + 1 + FftLaunchB<4>::G - 1) / FftLaunchB<4>::G;
+    case 8: return (8 / 2 + 1 + FftLaunchB<8>::G - 1) / FftLaunchB<8>::G;
+    case 16: return (16 / 2 + 1 + FftLaunchB<16>::G - 1) / FftLaunchB<16>::G;
+    case 32: return (32 / 2 + 1 + FftLaunchB<32>::G - 1) / FftLaunchB<32>::G;
+    case 64: return (64 / 2 + 1 + FftLaunchB<64>::G - 1) / FftLaunchB<64>::G;
+    case 128: return (128 / 2 + 1 + FftLaunchB<128>::G - 1) / FftLaunchB<128>::G;
+    case 256: return (256 / 2 + 1 + FftLaunchB<256>::G - 1) / FftLaunchB<256>::G;
+    case 512: return (512 / 2 + 1 + FftLaunchB<512>::G - 1) / FftLaunchB<512>::G;
+    case 1024: return (1024 / 2 + 1 + FftLaunchB<1024>::G - 1) / FftLaunchB<1024>::G;
+    case 2048: return (2048 / 2 + 1 + FftLaunchB<2048>::G - 1) / FftLaunchB<2048>::G;
+    case 4096: return (4096 / 2 + 1 + FftLaunchB<4096>::G - 1) / FftLaunchB<4096>::G;
   }
   return 0;
 }

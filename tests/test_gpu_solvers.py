@@ -72,6 +72,19 @@ def test_cg_fp32(cuda_lib, ci):
     assert solvers.objective(T, b[0], x[0]) <= solvers.objective(T, b[0], xk)
 
 
+@pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
+def test_fused_equals_unfused(cuda_lib, solver, monkeypatch):
+    """The fused 3-launch iteration (cg.cu) against the 5-launch one (solver.cu)."""
+    cfg = CONFIGS[2].with_(N=96, n_angles=60, n_det=137, ellipse_scale=1.5)
+    T = gram_taps(cfg.geometry())
+    b = rhs(cfg, T, B=2)
+    xf, hf = run(cuda_lib, cfg, b, 8, solver, B=2)
+    monkeypatch.setenv("BSCT_SOLVER_V1", "1")
+    xu, hu = run(cuda_lib, cfg, b, 8, solver, B=2)
+    assert rel_l2(xf, xu) < 1e-5
+    assert rel_l2(hf, hu) < 1e-5
+
+
 def test_batched_equals_single(cuda_lib):
     cfg = CONFIGS[2].with_(N=64, n_angles=60, n_det=91, ellipse_scale=1.0)
     T = gram_taps(cfg.geometry())
