@@ -75,6 +75,7 @@ struct bsct_plan_s {
   BPAngle *bp_ang = nullptr;  // K4 v2 per-angle parameters
   void *bp_B = nullptr;       // K4 v2 basis table
   int bp_cells = 0;           // K4 v2 tile cell capacity (0: use K4 v1)
+  int bp_maxp = 9;            // K4 v2 sub-intervals per detector cell (max over angles)
   bool solver_v1 = false;     // unfused 5-launch iteration (A/B testing only)
   void *T1 = nullptr, *gt = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
   void *sino_dev = nullptr, *b_dev = nullptr, *x_dev = nullptr;  // reconstruct_host staging
@@ -170,16 +171,61 @@ bsct_status gram_build_t(const bsct_geometry *g, int a0, int a1, T *taps, cudaSt
     CU(cudaMemsetAsync(taps, 0, D2 * sizeof(T), s));
     return BSCT_OK;
   }
+  static std::once_flag pool_once;
+  std::call_once(pool_once, [] {  // keep stream-ordered scratch in the pool between calls
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+  });
+  const char *dense_env = getenv("BSCT_GRAM_DENSE");
+  const bool dense = dense_env && dense_env[0] == '1';
+  // angles of the shard sorted by theta mod pi (window search of the windowed K1)
+  const double pi = 3.141592653589793238462643383279502884;
+  std::vector<std::pair<double, double>> srt(n);
+  for (int i = 0; i < n; ++i) {
+    const double t = g->angles[a0 + i];
+    srt[i] = {t - pi * std::floor(t / pi), t};
+  }
+  if (!dense) std::stable_sort(srt.begin(), srt.end(), [](auto &x, auto &y) { return x.first < y.first; });
+  std::vector<double> host(2 * (size_t)n);
+  for (int i = 0; i < n; ++i) {
+    host[i] = srt[i].second;
+    host[n + i] = std::min(std::max(srt[i].first, 0.0), std::nextafter(pi, 0.0));
+  }
   double *ang = nullptr;
   void *mem = nullptr;
-  CU(cudaMallocAsync((void **)&ang, sizeof(double) * n, s));
+  bool ang_owned = false;
+  {
+    // device copies of angle sets are cached by content: repeated builds of the same
+    // geometry enqueue no host->device copy (and so never wait on the stream)
+    static std::mutex mu;
+    static std::vector<std::pair<std::pair<int, std::vector<double>>, double *>> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    int dev = 0;
+    CU(cudaGetDevice(&dev));
+    for (auto &e : cache)
+      if (e.first.first == dev && e.first.second == host) ang = e.second;
+    if (!ang) {
+      CU(cudaMalloc((void **)&ang, sizeof(double) * 2 * n));
+      CU(cudaMemcpy(ang, host.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
+      if (cache.size() < 256) cache.push_back({{dev, host}, ang});
+      else ang_owned = true;
+    }
+  }
   CU(cudaMallocAsync(&mem, tables_bytes<T>(n), s));
-  CU(cudaMemcpyAsync(ang, g->angles + a0, sizeof(double) * n, cudaMemcpyHostToDevice, s));
   PPTables<T> tb = tables_of<T>(mem, n);
   CU(build_pp_tables<T>(ang, n, PP_GRAM, g->lambda_x, g->lambda_y, g->zeta_blur, tb, s));
-  CU(gram_taps<T>(N, g->lambda_x, n, tb.cs, tb.view(), taps, s));
+  if (dense) {
+    CU(gram_taps<T>(N, g->lambda_x, n, tb.cs, tb.view(), taps, s));
+  } else {
+    const double Hmax = (g->lambda_x * 1.4142135623730951 + g->zeta_blur) * (1.0 + 1e-12);
+    CU(gram_taps_window<T>(N, g->lambda_x, n, ang + n, tb.cs, tb.view(), Hmax, taps, s));
+  }
   CU(cudaFreeAsync(mem, s));
-  CU(cudaFreeAsync(ang, s));
+  if (ang_owned) CU(cudaFreeAsync(ang, s));
   return BSCT_OK;
 }
 
@@ -272,7 +318,7 @@ bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t 
   if (p->bp_cells > 0)
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject_v2<T>(p->N, p->n_angles, p->M, B, p->bp_ang, (const T *)p->bp_B, (const T *)p->gt, b,
-                              p->bp_cells, p->lx * p->lx * p->ly, s)));
+                              p->bp_cells, p->bp_maxp, p->lx * p->lx * p->ly, s)));
   else
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, bp.cs, bp.view(), (const T *)p->gt, b, s)));
@@ -379,6 +425,7 @@ bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *
   p->zeta = g->zeta_blur;
   p->dt = dt;
   p->max_batch = max_batch;
+  p->bp_maxp = bp_v2_max_p(g->n_angles, g->angles, g->lambda_x, g->lambda_y, g->zeta_blur);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMalloc((void **)&p->angles, sizeof(double) * g->n_angles);
   if (e == cudaSuccess) e = cudaMemcpyAsync(p->angles, g->angles, sizeof(double) * g->n_angles, cudaMemcpyHostToDevice, s);

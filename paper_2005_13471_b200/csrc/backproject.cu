@@ -9,6 +9,9 @@
 //     with widths [l|c|, l|s|, zeta] U [lambda_y]^(d+1) (the pixel footprint convolved with
 //     the degree-d B-spline interpolant, Eq.(1)); only the <= floor(W/lambda_y)+1 samples
 //     inside C_t's support contribute.
+#include <algorithm>
+#include <cmath>
+
 #include "kernels.cuh"
 #include "pptable.cuh"
 
@@ -276,14 +279,60 @@ __device__ __forceinline__ T horner6(const T *e, T t) {
   return r;
 }
 
-template <typename T>
+// 16-byte shared-memory vector of T (float4 / double2x2 halves)
+template <typename T> struct Vec8;
+template <> struct Vec8<float> {
+  __device__ static void load(const float *p, float *v) {
+    const float4 a = reinterpret_cast<const float4 *>(p)[0], b = reinterpret_cast<const float4 *>(p)[1];
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ static void store(float *p, const float *v) {
+    reinterpret_cast<float4 *>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4 *>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+template <> struct Vec8<double> {
+  __device__ static void load(const double *p, double *v) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 a = reinterpret_cast<const double2 *>(p)[i];
+      v[2 * i] = a.x; v[2 * i + 1] = a.y;
+    }
+  }
+  __device__ static void store(double *p, const double *v) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) reinterpret_cast<double2 *>(p)[i] = make_double2(v[2 * i], v[2 * i + 1]);
+  }
+};
+
+struct BPTileAngle {  // per (tile, angle) parameters
+  int c_lo, ncell;
+};
+__device__ __forceinline__ BPTileAngle bp_tile_angle(const BPAngle &A, int tk1, int tk2, int max_cells) {
+  const double ua = fma(A.du1, (double)tk1, fma(A.du2, (double)tk2, A.u0));
+  const double e1 = A.du1 * (BPT - 1), e2 = A.du2 * (BPT - 1);
+  const double umin = ua + fmin(0.0, e1) + fmin(0.0, e2), umax = ua + fmax(0.0, e1) + fmax(0.0, e2);
+  BPTileAngle r;
+  r.c_lo = (int)floor(umin) - 1;
+  r.ncell = min((int)floor(umax) - r.c_lo + 2, max_cells);
+  return r;
+}
+
+// Shared memory per buffer (double-buffered by angle parity):
+//   table [max_cells][maxP*8+4]  entries {c0..c5, bp_p, 0}; the odd number of 16-byte units per
+//                                 cell row keeps consecutive cells in distinct bank groups
+//   Bst   [maxP][BP_SMAX][8]     this angle's basis B[p][i][k]
+//   gst   [max_cells + BP_SMAX]  this tile's segment of g~
+// PC = compile-time number of breakpoint compares (>= maxP - 1; unused breakpoints are +huge).
+template <typename T, int PC>
 __global__ void __launch_bounds__(BP_THREADS) bp_v2_kernel(int N, int n_angles, int M, const BPAngle *__restrict__ ang,
                                                            const T *__restrict__ Btab, const T *__restrict__ gt,
-                                                           T *__restrict__ out, int max_cells, T scale) {
+                                                           T *__restrict__ out, int max_cells, int maxP, T scale) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *tab = reinterpret_cast<T *>(smem_raw);                       // [2][max_cells * (BP_PMAX/.. stride)]
-  __shared__ T sbp[2][BP_PMAX];
-  const int tstride = max_cells * (9 * 8 + 4);
+  T *sm = reinterpret_cast<T *>(smem_raw);
+  const int tab_sz = max_cells * (maxP * 8 + 4);
+  const int bst_sz = maxP * BP_SMAX * 8;
+  const int buf_sz = tab_sz + bst_sz + ((max_cells + BP_SMAX + 7) & ~7);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tk1 = blockIdx.y * BPT, tk2 = blockIdx.x * BPT;
   const int k1_0 = tk1 + (warp >> 1) * BP_ROWS;
@@ -291,48 +340,67 @@ __global__ void __launch_bounds__(BP_THREADS) bp_v2_kernel(int N, int n_angles, 
   const int b = blockIdx.z;
   const int Mt = M + 2 * HC;
   const T *g = gt + (size_t)b * n_angles * Mt;
+
+  // stage angle a's basis and g~ segment into buffer a & 1
+  auto stage = [&](int a) {
+    const BPAngle &A = ang[a];
+    const BPTileAngle ta = bp_tile_angle(A, tk1, tk2, max_cells);
+    T *base = sm + (a & 1) * buf_sz;
+    T *Bst = base + tab_sz;
+    T *gst = Bst + bst_sz;
+    const T *Ba = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
+    const int nb = A.P * BP_SMAX * 8;
+    for (int i = threadIdx.x * 4; i < nb; i += BP_THREADS * 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) Bst[i + u] = Ba[i + u];
+    }
+    const T *ga = g + (size_t)a * Mt + HC;  // ga[m]: g~ at detector index m in [-HC, M+HC)
+    const int m0 = ta.c_lo + A.imin;
+    for (int j = threadIdx.x; j < ta.ncell + A.S; j += BP_THREADS) {
+      const int m = m0 + j;
+      gst[j] = (m >= -HC && m < M + HC) ? ga[m] : (T)0;
+    }
+  };
+
   T acc[BP_ROWS];
 #pragma unroll
   for (int j = 0; j < BP_ROWS; ++j) acc[j] = 0;
+  stage(0);
+  __syncthreads();
   for (int a = 0; a < n_angles; ++a) {
     const BPAngle &A = ang[a];
-    const double u0 = A.u0, du1 = A.du1, du2 = A.du2;
-    const int P = A.P, S = A.S, imin = A.imin;
-    // tile cell range from its corners
-    const double ua = fma(du1, (double)tk1, fma(du2, (double)tk2, u0));
-    const double e1 = du1 * (BPT - 1), e2 = du2 * (BPT - 1);
-    const double umin = ua + fmin(0.0, e1) + fmin(0.0, e2), umax = ua + fmax(0.0, e1) + fmax(0.0, e2);
-    const int c_lo = (int)floor(umin) - 1;
-    const int ncell = min((int)floor(umax) - c_lo + 2, max_cells);
+    const int P = A.P, S = A.S;
+    const BPTileAngle ta = bp_tile_angle(A, tk1, tk2, max_cells);
     const int stride = P * 8 + 4;
-    T *buf = tab + (a & 1) * tstride;
-    if (threadIdx.x < BP_PMAX) sbp[a & 1][threadIdx.x] = (T)A.bp[threadIdx.x];
-    const T *Ba = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
-    const T *ga = g + (size_t)a * Mt + HC;  // ga[m] = g~ at detector index m (m in [-HC, M+HC))
-    for (int item = threadIdx.x; item < P * ncell; item += BP_THREADS) {
-      const int p = item / ncell, cc = item - p * ncell;
-      const int c0 = c_lo + cc + imin;
-      T f[6] = {0, 0, 0, 0, 0, 0};
-      const T *Bp = Ba + (size_t)p * BP_SMAX * 8;
+    T *buf = sm + (a & 1) * buf_sz;
+    const T *Bst = buf + tab_sz;
+    const T *gst = Bst + bst_sz;
+    // build F[c][p][k] = sum_i g~[c + i + imin] B[p][i][k] for the tile's cells
+    for (int item = threadIdx.x; item < P * ta.ncell; item += BP_THREADS) {
+      const int p = item / ta.ncell, cc = item - p * ta.ncell;
+      T f[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      const T *Bp = Bst + p * BP_SMAX * 8;
       for (int i = 0; i < S; ++i) {
-        const int m = c0 + i;
-        if (m < -HC || m >= M + HC) continue;
-        const T gv = ga[m];
-        const T *Bi = Bp + i * 8;
+        const T gv = gst[cc + i];
+        T bb[8];
+        Vec8<T>::load(Bp + i * 8, bb);
 #pragma unroll
-        for (int k = 0; k < 6; ++k) f[k] = fma(gv, Bi[k], f[k]);
+        for (int k = 0; k < 6; ++k) f[k] = fma(gv, bb[k], f[k]);
       }
-      T *e = buf + cc * stride + p * 8;
-#pragma unroll
-      for (int k = 0; k < 6; ++k) e[k] = f[k];
+      f[6] = (T)A.bp[p];
+      Vec8<T>::store(buf + cc * stride + p * 8, f);
     }
+    if (a + 1 < n_angles) stage(a + 1);  // the other buffer: last read before the previous barrier
     __syncthreads();
-    const T *bpv = sbp[a & 1];
-    const double ub = fma(du1, (double)k1_0, fma(du2, (double)k2, u0));
+    // evaluate: cell, sub-interval (uniform breakpoints in registers), one Horner
+    T bk[BP_PMAX];
+#pragma unroll
+    for (int k = 1; k <= PC; ++k) bk[k] = (T)A.bp[k];
+    const double ub = fma(A.du1, (double)k1_0, fma(A.du2, (double)k2, A.u0));
     const double cb = floor(ub);
     const T fb = (T)(ub - cb);
-    const int cbi = (int)cb - c_lo;
-    const T d1 = (T)du1;
+    const int cbi = (int)cb - ta.c_lo;
+    const T d1 = (T)A.du1;
 #pragma unroll
     for (int j = 0; j < BP_ROWS; ++j) {
       const T v = fma(d1, (T)j, fb);
@@ -340,12 +408,18 @@ __global__ void __launch_bounds__(BP_THREADS) bp_v2_kernel(int N, int n_angles, 
       const T ph = v - cf;
       const int cc = cbi + (int)cf;
       int p = 0;
-      if (bpv[p + 8] <= ph) p += 8;
-      if (bpv[p + 4] <= ph) p += 4;
-      if (bpv[p + 2] <= ph) p += 2;
-      if (bpv[p + 1] <= ph) p += 1;
-      const T tau = (T)(ph - bpv[p]);
-      acc[j] += horner6<T>(buf + cc * stride + p * 8, tau);
+#pragma unroll
+      for (int k = 1; k <= PC; ++k) p += (ph >= bk[k]) ? 1 : 0;
+      T e[8];
+      Vec8<T>::load(buf + cc * stride + p * 8, e);
+      const T tau = ph - e[6];
+      T rr = e[5];
+      rr = fma(rr, tau, e[4]);
+      rr = fma(rr, tau, e[3]);
+      rr = fma(rr, tau, e[2]);
+      rr = fma(rr, tau, e[1]);
+      rr = fma(rr, tau, e[0]);
+      acc[j] += rr;
     }
   }
   if (k2 < N) {
@@ -358,13 +432,73 @@ __global__ void __launch_bounds__(BP_THREADS) bp_v2_kernel(int N, int n_angles, 
 
 template <typename T>
 cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
-                           int max_cells, double scale, cudaStream_t s) {
-  const size_t sm = sizeof(T) * 2 * (size_t)max_cells * (9 * 8 + 4);
-  cudaError_t e = cudaFuncSetAttribute(bp_v2_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-  if (e != cudaSuccess) return e;
+                           int max_cells, int maxP, double scale, cudaStream_t s) {
+  const int tab_sz = max_cells * (maxP * 8 + 4);
+  const int buf_sz = tab_sz + maxP * BP_SMAX * 8 + ((max_cells + BP_SMAX + 7) & ~7);
+  const size_t sm = sizeof(T) * 2 * (size_t)buf_sz;
   dim3 grid((N + BPT - 1) / BPT, (N + BPT - 1) / BPT, B);
-  bp_v2_kernel<T><<<grid, BP_THREADS, sm, s>>>(N, n_angles, M, ang, Btab, gt, b, max_cells, (T)scale);
+  cudaError_t e;
+  if (maxP <= 5) {
+    e = cudaFuncSetAttribute(bp_v2_kernel<T, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    bp_v2_kernel<T, 4><<<grid, BP_THREADS, sm, s>>>(N, n_angles, M, ang, Btab, gt, b, max_cells, maxP, (T)scale);
+  } else {
+    e = cudaFuncSetAttribute(bp_v2_kernel<T, 8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    bp_v2_kernel<T, 8><<<grid, BP_THREADS, sm, s>>>(N, n_angles, M, ang, Btab, gt, b, max_cells, maxP, (T)scale);
+  }
   return cudaGetLastError();
+}
+
+// Host replica of the breakpoint count of bp_tables_kernel (sizes the shared memory; merges
+// with a tighter tolerance than the device, so it never under-counts).
+int bp_v2_max_p(int n, const double *angles, double lx, double ly, double zeta) {
+  int best = 1;
+  for (int a = 0; a < n; ++a) {
+    const double c = std::cos(angles[a]), s = std::sin(angles[a]);
+    double raw[8];
+    int nr = 0;
+    raw[nr++] = lx * std::fabs(c);
+    raw[nr++] = lx * std::fabs(s);
+    if (zeta > 0) raw[nr++] = zeta;
+    const int nbr = nr;
+    double s3 = 0;
+    for (int i = 0; i < nr; ++i) s3 += raw[i];
+    const double thr3 = 1e-12 * std::fmax(1.0, s3);
+    int nz = 0;
+    for (int i = 0; i < nr; ++i) nz += raw[i] > thr3;
+    for (int i = 0; i < nz; ++i) raw[nr++] = ly;
+    double ssum = 0;
+    for (int i = 0; i < nr; ++i) ssum += raw[i];
+    const double thr = 1e-12 * std::fmax(1.0, ssum);
+    double wb[3], W = 0;
+    int kb = 0;
+    for (int i = 0; i < nr; ++i)
+      if (raw[i] > thr) {
+        W += raw[i];
+        if (i < nbr) wb[kb++] = raw[i];
+      }
+    const double H = 0.5 * W;
+    double f[9];
+    int nf = 0;
+    f[nf++] = 0.0;
+    for (int m = 0; m < (1 << kb); ++m) {
+      double sg = 0;
+      for (int i = 0; i < kb; ++i)
+        if ((m >> i) & 1) sg += wb[i];
+      double v = (H - sg) / ly;
+      v -= std::floor(v);
+      if (v > 1.0 - 1e-13) v = 0.0;
+      f[nf++] = v;
+    }
+    std::sort(f, f + nf);
+    int np = 0;
+    double last = -1;
+    for (int i = 0; i < nf; ++i)
+      if (np == 0 || f[i] > last + 1e-13) { last = f[i]; ++np; }
+    best = np > best ? np : best;
+  }
+  return best > 9 ? 9 : best;
 }
 
 int bp_v2_max_cells(double lx, double ly, double zeta) {
@@ -379,9 +513,9 @@ template cudaError_t build_bp_tables<float>(int, int, double, double, double, in
 template cudaError_t build_bp_tables<double>(int, int, double, double, double, int, const PPTables<double> &,
                                              BPAngle *, double *, cudaStream_t);
 template cudaError_t backproject_v2<float>(int, int, int, int, const BPAngle *, const float *, const float *, float *,
-                                           int, double, cudaStream_t);
+                                           int, int, double, cudaStream_t);
 template cudaError_t backproject_v2<double>(int, int, int, int, const BPAngle *, const double *, const double *,
-                                            double *, int, double, cudaStream_t);
+                                            double *, int, int, double, cudaStream_t);
 template cudaError_t correction_filter<float>(int, int, int, const int *, const float *, float *, cudaStream_t);
 template cudaError_t correction_filter<double>(int, int, int, const int *, const double *, double *, cudaStream_t);
 template cudaError_t backproject<float>(int, double, double, int, int, int, const double *, PPView<float>,

@@ -54,8 +54,38 @@ __global__ void __launch_bounds__(256) cg_init_kernel(long n, const T *__restric
   if (blockIdx.x == 0 && threadIdx.x == 0 && w.flags) w.flags[blockIdx.y] = 0;
 }
 
+// VW-wide (16-byte when VW = 16/sizeof(T)) global loads / stores
+template <typename T, int VW>
+__device__ __forceinline__ void vload(T *dst, const T *__restrict__ src) {
+  if constexpr (VW * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      const float4 v = *reinterpret_cast<const float4 *>(src);
+      dst[0] = v.x; dst[1] = v.y; dst[2] = v.z; dst[3] = v.w;
+    } else {
+      const double2 v = *reinterpret_cast<const double2 *>(src);
+      dst[0] = v.x; dst[1] = v.y;
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < VW; ++u) dst[u] = src[u];
+  }
+}
+template <typename T, int VW>
+__device__ __forceinline__ void vstore(T *dst, const T *src) {
+  if constexpr (VW * sizeof(T) == 16) {
+    if constexpr (sizeof(T) == 4) {
+      *reinterpret_cast<float4 *>(dst) = make_float4(src[0], src[1], src[2], src[3]);
+    } else {
+      *reinterpret_cast<double2 *>(dst) = make_double2(src[0], src[1]);
+    }
+  } else {
+#pragma unroll
+    for (int u = 0; u < VW; ++u) dst[u] = src[u];
+  }
+}
+
 // ---------------------------------------------------------------- pass A (CG): p-update fused with row DFTs
-template <typename T, int L>
+template <typename T, int L, int VW>
 __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N, int k, T *__restrict__ x,
                                                                           const T *__restrict__ r,
                                                                           T *__restrict__ p,
@@ -84,32 +114,43 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N,
   }
   const T be = (T)beta, al = (T)alpha_prev;
   const int row0 = blockIdx.x * 2 * G;
-  const int ra = row0 + 2 * g, rb = ra + 1;
   const size_t so = (size_t)b * N * N;
+  // streaming phase: x += a p_old, p = r + b p_old over the CTA's 2G rows, VW-wide accesses,
+  // p written into the groups' FFT buffers (row 2gg -> real part, 2gg+1 -> imaginary part)
+  T *smT = reinterpret_cast<T *>(smem);
+  for (int i = threadIdx.x; i < G * (L - N); i += blockDim.x) {  // zero padding columns [N, L)
+    const int gg = i / (L - N), j = N + i % (L - N);
+    smem[gg * Cf::SMEM + pidx(j)] = V{0, 0};
+  }
+  const int rows = min(2 * G, N - row0);
+  if (rows < 2 * G)
+    for (int i = threadIdx.x; i < (2 * G - rows) * N; i += blockDim.x) {  // rows beyond N
+      const int rr = rows + i / N, j = i % N;
+      smT[2 * ((rr >> 1) * Cf::SMEM + pidx(j)) + (rr & 1)] = 0;
+    }
+  const int nv = N / VW;
+  for (int i = threadIdx.x; i < rows * nv; i += blockDim.x) {
+    const int rr = i / nv, j = (i - rr * nv) * VW;
+    const size_t e = so + (size_t)(row0 + rr) * N + j;
+    T pv[VW], rv[VW], xv[VW];
+    vload<T, VW>(pv, p + e);
+    vload<T, VW>(rv, r + e);
+    vload<T, VW>(xv, x + e);
+#pragma unroll
+    for (int u = 0; u < VW; ++u) {
+      xv[u] = fma(al, pv[u], xv[u]);
+      pv[u] = fma(be, pv[u], rv[u]);
+      smT[2 * ((rr >> 1) * Cf::SMEM + pidx(j + u)) + (rr & 1)] = pv[u];
+    }
+    vstore<T, VW>(x + e, xv);
+    vstore<T, VW>(p + e, pv);
+  }
+  __syncthreads();
+  V *sm = smem + g * Cf::SMEM;
   V v[E];
 #pragma unroll
-  for (int rr = 0; rr < E; ++rr) {
-    const int j = t + rr * P;
-    T va = 0, vb = 0;
-    if (j < N) {
-      if (ra < N) {
-        const size_t i = so + (size_t)ra * N + j;
-        const T po = p[i];
-        x[i] = fma(al, po, x[i]);
-        va = fma(be, po, r[i]);
-        p[i] = va;
-      }
-      if (rb < N) {
-        const size_t i = so + (size_t)rb * N + j;
-        const T po = p[i];
-        x[i] = fma(al, po, x[i]);
-        vb = fma(be, po, r[i]);
-        p[i] = vb;
-      }
-    }
-    v[rr] = V{va, vb};
-  }
-  V *sm = smem + g * Cf::SMEM;
+  for (int rr = 0; rr < E; ++rr) v[rr] = sm[pidx(t + rr * P)];
+  __syncthreads();
   fft_group<T, L, false>(v, sm, tw, t);
   V *T1s = T1 + (size_t)b * Q * N;
   for (int idx = threadIdx.x; idx < Q * G; idx += blockDim.x) {
@@ -126,7 +167,7 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N,
 
 // ---------------------------------------------------------------- pass C: inverse row DFTs fused with the r update
 // MODE 0: CG (x deferred to pass A); 1: steepest descent; 2: Landweber (alpha = tau)
-template <typename T, int L, int MODE>
+template <typename T, int L, int MODE, int VW>
 __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_c_kernel(int N, int k, int gparts,
                                                                           const cplx<T> *__restrict__ T1,
                                                                           T *__restrict__ x, T *__restrict__ r,
@@ -184,31 +225,27 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_c_kernel(int N,
   for (int rr = 0; rr < E; ++rr) v[rr] = sm[pidx(t + rr * P)];
   __syncthreads();
   fft_group<T, L, true>(v, sm, tw, t);
-  const int ra = row0 + 2 * g, rb = ra + 1;
+  // streaming phase: r -= alpha (G d) (and x += alpha r for SD / Landweber), VW-wide accesses
   const size_t so = (size_t)b * N * N;
+  const T *smT = reinterpret_cast<const T *>(smem);
+  const int rows = min(2 * G, N - row0);
+  const int nv = N / VW;
   double acc = 0;
+  for (int i = threadIdx.x; i < rows * nv; i += blockDim.x) {
+    const int rr = i / nv, j = (i - rr * nv) * VW;
+    const size_t e = so + (size_t)(row0 + rr) * N + j;
+    T rv[VW], xv[VW];
+    vload<T, VW>(rv, r + e);
+    if (MODE != 0) vload<T, VW>(xv, x + e);
 #pragma unroll
-  for (int rr = 0; rr < E; ++rr) {
-    const int n = t + rr * P;
-    if (n < N) {
-      const V z = sm[pidx(n)];
-      if (ra < N) {
-        const size_t i = so + (size_t)ra * N + n;
-        const T ro = r[i];
-        if (MODE != 0) x[i] = fma(al, ro, x[i]);
-        const T rn = fma(-al, z.x, ro);
-        r[i] = rn;
-        acc += (double)rn * rn;
-      }
-      if (rb < N) {
-        const size_t i = so + (size_t)rb * N + n;
-        const T ro = r[i];
-        if (MODE != 0) x[i] = fma(al, ro, x[i]);
-        const T rn = fma(-al, z.y, ro);
-        r[i] = rn;
-        acc += (double)rn * rn;
-      }
+    for (int u = 0; u < VW; ++u) {
+      const T z = smT[2 * ((rr >> 1) * Cf::SMEM + pidx(j + u)) + (rr & 1)];
+      if (MODE != 0) xv[u] = fma(al, rv[u], xv[u]);
+      rv[u] = fma(-al, z, rv[u]);
+      acc += (double)rv[u] * rv[u];
     }
+    vstore<T, VW>(r + e, rv);
+    if (MODE != 0) vstore<T, VW>(x + e, xv);
   }
   const double s = cta_sum(acc, red);
   if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
@@ -266,39 +303,54 @@ static cudaError_t cg_set_smem(K kernel, size_t bytes) {
   return cudaSuccess;
 }
 
+// 16-byte vector accesses need N divisible by the vector width and 16-byte aligned bases
+template <typename T>
+static bool can_vec(int N, const void *a, const void *b, const void *c) {
+  constexpr int VW = 16 / sizeof(T);
+  auto al = [](const void *q) { return q == nullptr || ((uintptr_t)q & 15) == 0; };
+  return N % VW == 0 && al(a) && al(b) && al(c);
+}
+
+template <typename T, int L, int VW>
+static cudaError_t cg_pass_a_LV(int N, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
+                                FusedWork w, cudaStream_t s) {
+  const size_t sm = cg_smem<L>(sizeof(cplx<T>));
+  cudaError_t e = cg_set_smem(cg_pass_a_kernel<T, L, VW>, sm);
+  if (e != cudaSuccess) return e;
+  cg_pass_a_kernel<T, L, VW><<<dim3(w.nparts, B), FftLaunch<L>::THREADS, sm, s>>>(N, k, x, r, p, T1, tw, w);
+  return cudaGetLastError();
+}
 template <typename T, int L>
 static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
                                FusedWork w, cudaStream_t s) {
-  const size_t sm = cg_smem<L>(sizeof(cplx<T>));
-  cudaError_t e = cg_set_smem(cg_pass_a_kernel<T, L>, sm);
-  if (e != cudaSuccess) return e;
-  cg_pass_a_kernel<T, L><<<dim3(w.nparts, B), FftLaunch<L>::THREADS, sm, s>>>(N, k, x, r, p, T1, tw, w);
-  return cudaGetLastError();
+  if (can_vec<T>(N, x, r, p)) return cg_pass_a_LV<T, L, 16 / sizeof(T)>(N, B, k, x, r, p, T1, tw, w, s);
+  return cg_pass_a_LV<T, L, 1>(N, B, k, x, r, p, T1, tw, w, s);
 }
 
+template <typename T, int L, int MODE, int VW>
+static cudaError_t cg_pass_c_LMV(int N, int B, int k, int gparts, const cplx<T> *T1, T *x, T *r, const cplx<T> *tw,
+                                 FusedWork w, cudaStream_t s) {
+  const size_t sm = cg_smem<L>(sizeof(cplx<T>));
+  cudaError_t e = cg_set_smem(cg_pass_c_kernel<T, L, MODE, VW>, sm);
+  if (e != cudaSuccess) return e;
+  cg_pass_c_kernel<T, L, MODE, VW><<<dim3(w.nparts, B), FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r,
+                                                                                         tw, w);
+  return cudaGetLastError();
+}
+template <typename T, int L, int MODE>
+static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *T1, T *x, T *r, const cplx<T> *tw,
+                                FusedWork w, cudaStream_t s) {
+  if (can_vec<T>(N, x, r, nullptr)) return cg_pass_c_LMV<T, L, MODE, 16 / sizeof(T)>(N, B, k, gparts, T1, x, r, tw, w, s);
+  return cg_pass_c_LMV<T, L, MODE, 1>(N, B, k, gparts, T1, x, r, tw, w, s);
+}
 template <typename T, int L>
 static cudaError_t cg_pass_c_L(int N, int B, int k, int mode, int gparts, const cplx<T> *T1, T *x, T *r,
                                const cplx<T> *tw, FusedWork w, cudaStream_t s) {
-  const size_t sm = cg_smem<L>(sizeof(cplx<T>));
-  const dim3 grid(w.nparts, B);
-  cudaError_t e;
   switch (mode) {
-    case 0:
-      e = cg_set_smem(cg_pass_c_kernel<T, L, 0>, sm);
-      if (e != cudaSuccess) return e;
-      cg_pass_c_kernel<T, L, 0><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r, tw, w);
-      break;
-    case 1:
-      e = cg_set_smem(cg_pass_c_kernel<T, L, 1>, sm);
-      if (e != cudaSuccess) return e;
-      cg_pass_c_kernel<T, L, 1><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r, tw, w);
-      break;
-    default:
-      e = cg_set_smem(cg_pass_c_kernel<T, L, 2>, sm);
-      if (e != cudaSuccess) return e;
-      cg_pass_c_kernel<T, L, 2><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, k, gparts, T1, x, r, tw, w);
+    case 0: return cg_pass_c_LM<T, L, 0>(N, B, k, gparts, T1, x, r, tw, w, s);
+    case 1: return cg_pass_c_LM<T, L, 1>(N, B, k, gparts, T1, x, r, tw, w, s);
+    default: return cg_pass_c_LM<T, L, 2>(N, B, k, gparts, T1, x, r, tw, w, s);
   }
-  return cudaGetLastError();
 }
 
 #define CG_L_SWITCH(L, CALL)                             \

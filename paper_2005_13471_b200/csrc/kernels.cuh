@@ -45,6 +45,10 @@ cudaError_t build_pp_tables(const double *angles_dev, int n, int kind, double lx
 // K1 (gram.cu): taps[(2N-1)^2] = lx^4 sum_{a < n} M_a(lx <(-s_a, c_a), dk>)
 template <typename T>
 cudaError_t gram_taps(int N, double lx, int n, const double *cs, PPView<T> tb, T *taps, cudaStream_t s);
+// windowed K1: angles sorted mod pi (theta_sorted ascending in [0, pi)); Hmax >= max_t W_t/2
+template <typename T>
+cudaError_t gram_taps_window(int N, double lx, int n, const double *theta_sorted, const double *cs, PPView<T> tb,
+                             double Hmax, T *taps, cudaStream_t s);
 
 // K2 (normal.cu): S[q][p] = Re DFT2(E)[p][q] / L^2, work >= (L/2+1)*L complex
 template <typename T>
@@ -82,12 +86,13 @@ struct BPAngle {
 };
 size_t bp_table_floats(int n);  // size of the basis table B[n][BP_PMAX][BP_SMAX][8]
 int bp_v2_max_cells(double lx, double ly, double zeta);  // 0: geometry not supported by v2
+int bp_v2_max_p(int n, const double *angles, double lx, double ly, double zeta);  // host, sub-intervals per cell
 template <typename T>
 cudaError_t build_bp_tables(int N, int M, double lx, double ly, double zeta, int n, const PPTables<T> &tb,
                             BPAngle *ang, T *Btab, cudaStream_t s);
 template <typename T>
 cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
-                           int max_cells, double scale, cudaStream_t s);
+                           int max_cells, int maxP, double scale, cudaStream_t s);
 
 // K7 (forward.cu)
 template <typename T>

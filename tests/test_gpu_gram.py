@@ -58,6 +58,17 @@ def test_config4_sampled(cuda_lib):
     assert rel_l2(got, ref) < 1e-5
 
 
+@pytest.mark.parametrize("ci", [2, 4])
+def test_window_equals_dense(cuda_lib, ci, monkeypatch):
+    """Windowed K1 (angle window per tap) against the dense angle loop."""
+    g = CONFIGS[ci].geometry()
+    win = to_np(gpu_taps(cuda_lib, g, "f32"))
+    monkeypatch.setenv("BSCT_GRAM_DENSE", "1")
+    dense = to_np(gpu_taps(cuda_lib, g, "f32"))
+    assert rel_l2(win, dense) < 1e-6
+    assert np.array_equal(win == 0, dense == 0)
+
+
 def test_angle_shards_sum(cuda_lib):
     """BJ:configs[4]: angle-sharded partial filters sum to the full filter."""
     import torch
