@@ -6,6 +6,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/bsct.h"
@@ -77,6 +78,7 @@ struct bsct_plan_s {
   int bp_cells = 0;           // K4 v2 tile cell capacity (0: use K4 v1)
   int bp_maxp = 9;            // K4 v2 sub-intervals per detector cell (max over angles)
   bool solver_v1 = false;     // unfused 5-launch iteration (A/B testing only)
+  bool bp_v3 = true;          // FP32: K4 v3 (slices per CTA); BSCT_BP_V2=1 selects v2 (A/B testing)
   void *T1 = nullptr, *gt = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
   void *sino_dev = nullptr, *b_dev = nullptr, *x_dev = nullptr;  // reconstruct_host staging
   double *alpha = nullptr, *gpart = nullptr, *rpart = nullptr, *tau = nullptr;
@@ -262,6 +264,8 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc((void **)&p->tau, sizeof(double)));
   const char *force_v1 = getenv("BSCT_BP_V1");
   p->bp_cells = (force_v1 && force_v1[0] == '1') ? 0 : bp_v2_max_cells(p->lx, p->ly, p->zeta);
+  const char *bp2 = getenv("BSCT_BP_V2");
+  p->bp_v3 = !(bp2 && bp2[0] == '1');
   if (p->bp_cells > 0) {
     CU(cudaMalloc((void **)&p->bp_ang, sizeof(BPAngle) * n));
     CU(cudaMalloc(&p->bp_B, sizeof(T) * bp_table_floats(n)));
@@ -315,7 +319,13 @@ template <typename T>
 bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t s) {
   PPTables<T> bp = tables_of<T>(p->bp_mem, p->n_angles);
   LAUNCH(p, BSCT_K_CORRECTION, 1, (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s)));
-  if (p->bp_cells > 0)
+  const int sb = (p->bp_cells > 0 && p->bp_v3 && std::is_same<T, float>::value)
+                     ? bp_v3_slices(B, p->bp_maxp, p->bp_cells) : 0;
+  if (sb > 0) {
+    LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+           (backproject_v3(p->N, p->n_angles, p->M, B, p->bp_ang, (const float *)p->bp_B, (const float *)p->gt,
+                           (float *)b, p->bp_cells, p->bp_maxp, p->lx * p->lx * p->ly, sb, s)));
+  } else if (p->bp_cells > 0)
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject_v2<T>(p->N, p->n_angles, p->M, B, p->bp_ang, (const T *)p->bp_B, (const T *)p->gt, b,
                               p->bp_cells, p->bp_maxp, p->lx * p->lx * p->ly, s)));
@@ -323,6 +333,25 @@ bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t 
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, bp.cs, bp.view(), (const T *)p->gt, b, s)));
   return BSCT_OK;
+}
+
+// Slices per solver chunk: the per-iteration working set of a chunk (x, r, p and the FFT
+// intermediate T1) is kept below an L2 budget (default 72 MB of the 126 MB L2;
+// BSCT_L2_BUDGET_MB overrides, BSCT_CG_CHUNK forces a chunk size, 0 = whole batch).
+int solver_chunk(bsct_plan p, int B) {
+  if (const char *e = getenv("BSCT_CG_CHUNK")) {
+    const int c = atoi(e);
+    return c <= 0 ? std::max(B, 1) : std::min(c, std::max(B, 1));
+  }
+  // Measured on B200 (config 5): chunks of 6-24 slices were 1.3-2x slower than one
+  // whole-batch pass (the passes are issue/latency bound, and small grids add tails),
+  // so chunking is opt-in: BSCT_L2_BUDGET_MB enables it.
+  double budget = 0.0;
+  if (const char *e = getenv("BSCT_L2_BUDGET_MB")) budget = atof(e);
+  if (budget <= 0) return std::max(B, 1);
+  const double per = (double)p->esize() * (3.0 * p->N * p->N + 2.0 * (p->L / 2 + 1) * p->N);
+  const int c = (int)(budget * 1048576.0 / per);
+  return std::max(1, std::min(c, std::max(B, 1)));
 }
 
 template <typename T>
@@ -336,33 +365,44 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
   }
   T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
   if (!p->solver_v1) {
-    // fused iteration (cg.cu): 3 launches per iteration
-    FusedWork fw;
-    fw.rho = p->rho;
-    fw.rho_stride = iters + 1;
-    fw.alpha = p->alpha;
-    fw.gpart = p->gpart;
-    fw.rpart = p->rpart;
-    fw.nparts = fused_parts(p->N, p->L);
-    fw.B = B;
-    fw.flags = flags ? flags : p->flags;
-    fw.resid = resid;
-    fw.iters = iters;
-    fw.tau = p->tau;
+    // fused iteration (cg.cu): 3 launches per iteration.  Slices are solved in chunks whose
+    // per-iteration working set (x, r, p, T1) stays resident in L2, so that the FFT
+    // intermediates and the CG vectors cycle through L2 instead of HBM.
+    const int nparts = fused_parts(p->N, p->L);
+    const int cb = solver_chunk(p, B);
     auto *T1 = (cplx<T> *)p->T1;
     auto *tw = (const cplx<T> *)p->tw;
     const int gparts = pass_b_blocks(p->L);
-    LAUNCH(p, BSCT_K_SOLVER_INIT, 1, (fused_init<T>(p->N, B, b, x, r, solver == BSCT_CG ? pp : (T *)nullptr, fw, s)));
-    for (int it = 0; it < iters; ++it) {
-      if (solver == BSCT_CG)
-        LAUNCH(p, BSCT_K_PASS_A, 1, (fused_pass_a<T>(p->N, p->L, B, it, x, r, pp, T1, tw, fw, s)));
-      else
-        LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, B, r, T1, tw, s)));
-      LAUNCH(p, BSCT_K_PASS_B, 1,
-             (pass_b<T>(p->N, p->L, B, T1, (const T *)p->S, tw, solver == BSCT_LANDWEBER ? nullptr : p->gpart, s)));
-      LAUNCH(p, BSCT_K_PASS_C, 1, (fused_pass_c<T>(p->N, p->L, B, it, solver, gparts, T1, x, r, tw, fw, s)));
+    const size_t nn = (size_t)p->N * p->N;
+    for (int c0 = 0; c0 < B; c0 += cb) {
+      const int nb = std::min(cb, B - c0);
+      const T *bc = b + c0 * nn;
+      T *xc = x + c0 * nn;
+      FusedWork fw;
+      fw.rho = p->rho + (size_t)c0 * (iters + 1);
+      fw.rho_stride = iters + 1;
+      fw.alpha = p->alpha + c0;
+      fw.gpart = p->gpart;
+      fw.rpart = p->rpart;
+      fw.nparts = nparts;
+      fw.B = nb;
+      fw.flags = (flags ? flags : p->flags) + c0;
+      fw.resid = resid ? resid + (size_t)c0 * iters : nullptr;
+      fw.iters = iters;
+      fw.tau = p->tau;
+      LAUNCH(p, BSCT_K_SOLVER_INIT, 1,
+             (fused_init<T>(p->N, nb, bc, xc, r, solver == BSCT_CG ? pp : (T *)nullptr, fw, s)));
+      for (int it = 0; it < iters; ++it) {
+        if (solver == BSCT_CG)
+          LAUNCH(p, BSCT_K_PASS_A, 1, (fused_pass_a<T>(p->N, p->L, nb, it, xc, r, pp, T1, tw, fw, s)));
+        else
+          LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, nb, r, T1, tw, s)));
+        LAUNCH(p, BSCT_K_PASS_B, 1,
+               (pass_b<T>(p->N, p->L, nb, T1, (const T *)p->S, tw, solver == BSCT_LANDWEBER ? nullptr : p->gpart, s)));
+        LAUNCH(p, BSCT_K_PASS_C, 1, (fused_pass_c<T>(p->N, p->L, nb, it, solver, gparts, T1, xc, r, tw, fw, s)));
+      }
+      LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, nb, iters, solver == BSCT_CG, xc, pp, fw, s)));
     }
-    LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, B, iters, solver == BSCT_CG, x, pp, fw, s)));
     return BSCT_OK;
   }
   SolverWork w = solver_work(p, resid, flags);

@@ -450,6 +450,233 @@ cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang
   return cudaGetLastError();
 }
 
+// ----------------------------------------------------------------------------------------
+// K4 v3 (FP32): SB slices per CTA.  The per-(tile, angle) geometry -- which cell and which
+// sub-interval each pixel falls in, and tau -- depends only on the angle, so one locate per
+// pixel-angle serves SB slices; each slice then costs two 16-byte table loads and one
+// degree-5 Horner.  Table entries are interleaved by slice, [cell][p][s][8] = {c0..c5,
+// bp_p - 1/2, 0}, so the SB loads of one pixel use immediate offsets from one address.
+// The cell index uses round-to-nearest through the FP32 magic constant 1.5 * 2^23 on
+// u - 1/2 (no conversion instructions): ph - 1/2 = (u - 1/2) - round(u - 1/2), exact.
+// At ph = 1 (a tie rounded to even) the last sub-interval of the previous cell is
+// evaluated at its right end, which equals F at the cell start (F_t is continuous: the
+// box spline has >= 2 nonzero widths).  Same closed form as K4 v1/v2.
+// ----------------------------------------------------------------------------------------
+constexpr float BP_MAGIC = 12582912.0f;  // 1.5 * 2^23
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+// 4-byte copy; src_bytes = 0 writes a zero (src must still be a valid address)
+__device__ __forceinline__ void cp_async4(void *dst, const void *src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int NPEND>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(NPEND)); }
+
+// Shared memory: table double buffer [2][SB][6][PL] FP32 coefficient planes (entry
+// idx = cell * P + p, one float per plane) + a 3-slot staging ring [3][stg_sz] (basis of
+// the angle + the SB g~ segments) filled by cp.async two angles ahead, so that the
+// global-load latency overlaps a whole angle of work.  Each warp evaluates 4 x 8 pixel
+// blocks: with one 4-byte load per coefficient plane, a block's lanes hit ~1.4
+// wavefronts per load on average over the config-5 angles (vs ~7.4 per 16-byte load for
+// 32-pixel rows with 32-byte entries; bank model checked against ncu).  The sub-interval
+// start bp_p is selected from registers alongside the sub-interval search.
+template <int SB, int PC, int PL>
+__global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int n_angles, int M,
+                                                              const BPAngle *__restrict__ ang,
+                                                              const float *__restrict__ Btab,
+                                                              const float *__restrict__ gt, float *__restrict__ out,
+                                                              int max_cells, int maxP, float scale) {
+  constexpr int TAB = SB * 6 * PL;  // floats per table buffer
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *sm = reinterpret_cast<float *>(smem_raw);
+  const int bst_sz = maxP * BP_SMAX * 8;
+  const int gseg = (max_cells + BP_SMAX + 3) & ~3;
+  const int stg_sz = bst_sz + SB * gseg;
+  float *stg0 = sm + 2 * TAB;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tk1 = blockIdx.y * BPT, tk2 = blockIdx.x * BPT;
+  // warp w: columns 8w..8w+7 of the tile; lane: row (lane >> 3) of each 4-row block
+  const int k1_0 = tk1 + (lane >> 3);
+  const int k2 = tk2 + warp * 8 + (lane & 7);
+  const int b0 = blockIdx.z * SB;
+  const int Mt = M + 2 * HC;
+
+  auto stage = [&](int a) {  // asynchronous: basis + g~ segments of angle a into ring slot a % 3
+    if (a < n_angles) {
+      const BPAngle &A = ang[a];
+      const BPTileAngle ta = bp_tile_angle(A, tk1, tk2, max_cells);
+      float *Bst = stg0 + (a % 3) * stg_sz;
+      float *gst = Bst + bst_sz;
+      const float *Ba = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
+      const int nb4 = A.P * BP_SMAX * 2;
+      for (int i = threadIdx.x; i < nb4; i += BP_THREADS) cp_async16(Bst + 4 * i, Ba + 4 * i);
+      const int m0 = ta.c_lo + A.imin;
+      const int len = ta.ncell + A.S;
+      for (int j = threadIdx.x; j < SB * len; j += BP_THREADS) {
+        const int sl = j / len, jj = j - sl * len;
+        const int m = m0 + jj;
+        const bool ok = b0 + sl < B && m >= -HC && m < M + HC;
+        const float *src = ok ? gt + ((size_t)(b0 + sl) * n_angles + a) * Mt + HC + m : gt;
+        cp_async4(gst + sl * gseg + jj, src, ok ? 4 : 0);
+      }
+    }
+    cp_async_commit();  // (possibly empty) group per angle keeps the wait count uniform
+  };
+
+  float acc[SB][BP_ROWS];
+#pragma unroll
+  for (int sl = 0; sl < SB; ++sl)
+#pragma unroll
+    for (int j = 0; j < BP_ROWS; ++j) acc[sl][j] = 0.f;
+  stage(0);
+  stage(1);
+  cp_async_wait<1>();
+  __syncthreads();
+  for (int a = 0; a < n_angles; ++a) {
+    const BPAngle &A = ang[a];
+    const int P = A.P, S = A.S;
+    const BPTileAngle ta = bp_tile_angle(A, tk1, tk2, max_cells);
+    float *tab = sm + (a & 1) * TAB;
+    const float *Bst = stg0 + (a % 3) * stg_sz;
+    const float *gst = Bst + bst_sz;
+    // build F_s[c][p][k] = sum_i g~_s[c + i + imin] B[p][i][k] for the tile's cells, all SB slices
+    for (int item = threadIdx.x; item < P * ta.ncell; item += BP_THREADS) {
+      const int p = item / ta.ncell, cc = item - p * ta.ncell;
+      float f[SB][6];
+#pragma unroll
+      for (int sl = 0; sl < SB; ++sl)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) f[sl][k] = 0.f;
+      const float *Bp = Bst + p * BP_SMAX * 8;
+      for (int i = 0; i < S; ++i) {
+        float bb[8];
+        Vec8<float>::load(Bp + i * 8, bb);
+#pragma unroll
+        for (int sl = 0; sl < SB; ++sl) {
+          const float gv = gst[sl * gseg + cc + i];
+#pragma unroll
+          for (int k = 0; k < 6; ++k) f[sl][k] = fmaf(gv, bb[k], f[sl][k]);
+        }
+      }
+      float *dst = tab + cc * P + p;
+#pragma unroll
+      for (int sl = 0; sl < SB; ++sl)
+#pragma unroll
+        for (int k = 0; k < 6; ++k) dst[(sl * 6 + k) * PL] = f[sl][k];
+    }
+    // slot (a + 2) % 3 was last read by build(a - 1), before the previous barrier
+    stage(a + 2);
+    cp_async_wait<1>();  // this thread's copies of angle a + 1 have landed
+    __syncthreads();     // table(a) and staged(a + 1) visible to the CTA
+    // evaluate: one locate per pixel, 6 plane loads + one Horner per slice
+    float bkm[PC + 1];
+#pragma unroll
+    for (int k = 1; k <= PC; ++k) bkm[k] = (float)(A.bp[k] - 0.5);
+    const double ub = fma(A.du1, (double)k1_0, fma(A.du2, (double)k2, A.u0));
+    const double cb = floor(ub);
+    const float fbm = (float)(ub - cb) - 0.5f;
+    const float *tb = tab + ((int)cb - ta.c_lo) * P;
+    const float d4 = (float)(4.0 * A.du1);  // u step between the 4-row blocks
+#pragma unroll
+    for (int j = 0; j < BP_ROWS; ++j) {
+      const float w = fmaf(d4, (float)j, fbm);
+      const float t = w + BP_MAGIC;
+      const int ci = __float_as_int(t) - __float_as_int(BP_MAGIC);
+      const float phm = w - (t - BP_MAGIC);
+      int po = 0;
+      float bsel = -0.5f;  // bp_0 - 1/2
+#pragma unroll
+      for (int k = 1; k <= PC; ++k) {
+        const bool ge = phm >= bkm[k];
+        po += ge ? 1 : 0;
+        bsel = ge ? bkm[k] : bsel;
+      }
+      const float tau = phm - bsel;
+      const float *e = tb + ci * P + po;
+#pragma unroll
+      for (int sl = 0; sl < SB; ++sl) {
+        float rr = e[(sl * 6 + 5) * PL];
+        rr = fmaf(rr, tau, e[(sl * 6 + 4) * PL]);
+        rr = fmaf(rr, tau, e[(sl * 6 + 3) * PL]);
+        rr = fmaf(rr, tau, e[(sl * 6 + 2) * PL]);
+        rr = fmaf(rr, tau, e[(sl * 6 + 1) * PL]);
+        rr = fmaf(rr, tau, e[(sl * 6 + 0) * PL]);
+        acc[sl][j] += rr;
+      }
+    }
+  }
+  if (k2 < N) {
+#pragma unroll
+    for (int sl = 0; sl < SB; ++sl) {
+      if (b0 + sl >= B) break;
+      float *o = out + (size_t)(b0 + sl) * N * N;
+#pragma unroll
+      for (int j = 0; j < BP_ROWS; ++j)
+        if (k1_0 + 4 * j < N) o[(size_t)(k1_0 + 4 * j) * N + k2] = scale * acc[sl][j];
+    }
+  }
+}
+
+static int bp_v3_plane(int max_cells, int maxP) {
+  const int need = max_cells * maxP;
+  return need <= 512 ? 512 : need <= 1024 ? 1024 : need <= 2048 ? 2048 : 0;
+}
+
+static size_t bp_v3_smem(int SB, int max_cells, int maxP) {
+  const size_t PL = (size_t)bp_v3_plane(max_cells, maxP);
+  const size_t stg = (size_t)maxP * BP_SMAX * 8 + SB * (size_t)((max_cells + BP_SMAX + 3) & ~3);
+  return sizeof(float) * (2 * (size_t)SB * 6 * PL + 3 * stg);
+}
+
+template <int SB, int PC, int PL>
+static cudaError_t launch_bp_v3(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab,
+                                const float *gt, float *b, int max_cells, int maxP, float scale, cudaStream_t s) {
+  const size_t sm = bp_v3_smem(SB, max_cells, maxP);
+  if (sm > 227 * 1024 || max_cells * maxP > PL) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaFuncSetAttribute(bp_v3_kernel<SB, PC, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid((N + BPT - 1) / BPT, (N + BPT - 1) / BPT, (B + SB - 1) / SB);
+  bp_v3_kernel<SB, PC, PL><<<grid, BP_THREADS, sm, s>>>(N, B, n_angles, M, ang, Btab, gt, b, max_cells, maxP, scale);
+  return cudaGetLastError();
+}
+
+int bp_v3_slices(int B, int maxP, int max_cells) {
+  // slices per CTA (BSCT_BP_SB overrides; default 4, measured best on config 5: 285 ms vs
+  // 354 (SB = 2) and 495 (SB = 1)); 0 when no plane size fits (use K4 v2)
+  if (bp_v3_plane(max_cells, maxP) == 0) return 0;
+  int sb = B >= 4 ? 4 : B >= 2 ? 2 : 1;
+  if (const char *e = getenv("BSCT_BP_SB")) sb = atoi(e);
+  if (sb != 1 && sb != 2 && sb != 4) sb = 1;
+  while (sb > 1 && bp_v3_smem(sb, max_cells, maxP) > 227 * 1024) sb /= 2;
+  return bp_v3_smem(sb, max_cells, maxP) > 227 * 1024 ? 0 : sb;
+}
+
+cudaError_t backproject_v3(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
+                           float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s) {
+  const float sc = (float)scale;
+  const int PL = bp_v3_plane(max_cells, maxP);
+#define BP3(SBV, PLV)                                                                                         \
+  return maxP <= 5 ? launch_bp_v3<SBV, 4, PLV>(N, n_angles, M, B, ang, Btab, gt, b, max_cells, maxP, sc, s) \
+                   : launch_bp_v3<SBV, 8, PLV>(N, n_angles, M, B, ang, Btab, gt, b, max_cells, maxP, sc, s)
+#define BP3P(SBV)                        \
+  switch (PL) {                          \
+    case 512: BP3(SBV, 512);             \
+    case 1024: BP3(SBV, 1024);           \
+    case 2048: BP3(SBV, 2048);           \
+    default: return cudaErrorInvalidValue; \
+  }
+  if (SB == 4) { BP3P(4); }
+  if (SB == 2) { BP3P(2); }
+  BP3P(1);
+#undef BP3P
+#undef BP3
+}
+
 // Host replica of the breakpoint count of bp_tables_kernel (sizes the shared memory; merges
 // with a tighter tolerance than the device, so it never under-counts).
 int bp_v2_max_p(int n, const double *angles, double lx, double ly, double zeta) {

@@ -94,6 +94,11 @@ template <typename T>
 cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
                            int max_cells, int maxP, double scale, cudaStream_t s);
 
+// K4 v3 (FP32): SB in {1, 2, 4} slices per CTA share each pixel's locate
+int bp_v3_slices(int B, int maxP, int max_cells);
+cudaError_t backproject_v3(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
+                           float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s);
+
 // K7 (forward.cu)
 template <typename T>
 cudaError_t forward_project(int N, double lx, double ly, int n_angles, int M, int B, const double *cs,
