@@ -62,7 +62,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("BSCT_LIB") or LIB_PATH  # BSCT_LIB: A/B builds (tools/)
     if not os.path.exists(p):
         raise ImportError(f"{p} not found -- build it with `python -m paper_2005_13471_b200.build`")
     lib = ctypes.CDLL(p)

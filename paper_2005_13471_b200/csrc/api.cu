@@ -281,7 +281,7 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc(&p->p, sizeof(T) * nn * Bz));
   CU(cudaMalloc(&p->q, sizeof(T) * nn * Bz));
   CU(cudaMalloc((void **)&p->alpha, sizeof(double) * Bz));
-  CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * pass_b_blocks(L)));
+  CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * pass_b_blocks(L, p->dt == BSCT_F32)));
   const size_t nrp = std::max((size_t)vec_blocks(N), (size_t)2 * fused_parts(N, L));
   CU(cudaMalloc((void **)&p->rpart, sizeof(double) * Bz * nrp));
   const char *sv1 = getenv("BSCT_SOLVER_V1");
@@ -296,7 +296,7 @@ SolverWork solver_work(bsct_plan p, double *resid, int *flags) {
   w.rho = p->rho;
   w.alpha = p->alpha;
   w.gpart = p->gpart;
-  w.gstride = pass_b_blocks(p->L);
+  w.gstride = pass_b_blocks(p->L, p->dt == BSCT_F32);
   w.rpart = p->rpart;
   w.rstride = vec_blocks(p->N);
   w.flags = flags ? flags : p->flags;
@@ -372,7 +372,7 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     const int cb = solver_chunk(p, B);
     auto *T1 = (cplx<T> *)p->T1;
     auto *tw = (const cplx<T> *)p->tw;
-    const int gparts = pass_b_blocks(p->L);
+    const int gparts = pass_b_blocks(p->L, p->dt == BSCT_F32);
     const size_t nn = (size_t)p->N * p->N;
     for (int c0 = 0; c0 < B; c0 += cb) {
       const int nb = std::min(cb, B - c0);

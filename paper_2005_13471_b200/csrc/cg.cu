@@ -13,6 +13,10 @@
 // Partials of <r,r> are double-buffered by iteration parity so that a kernel may read the
 // previous partials while writing the next ones.
 #include "fft.cuh"
+#include "fft32.cuh"
+
+#include <cstdlib>
+#include <type_traits>
 #include "kernels.cuh"
 
 namespace bsct {
@@ -251,6 +255,137 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_c_kernel(int N,
   if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
 }
 
+// ---------------------------------------------------------------- pass C, L = 1024 (FP32 warp FFTs)
+// Same contract as cg_pass_c_kernel (16 rows per CTA, the same rpart layout).  The 16 rows'
+// T1 entries are staged by cp.async into shared memory as [q][9] row-pair float4 slots
+// (9: the eight lanes of a quarter warp reading consecutive q hit distinct bank groups),
+// each warp inverts one row pair with a 32 x 32 four-step FFT (fft32.cuh) forming only the
+// first N <= 512 outputs, and updates r (and x) in place; its r (x) rows are loaded into
+// registers before the FFT so that their latency overlaps the arithmetic.
+__device__ __forceinline__ void cp_async16_g(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(src));
+}
+__device__ __forceinline__ void cp_async8_g(void *dst, const void *src) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, int gparts,
+                                                                const float2 *__restrict__ T1,
+                                                                float *__restrict__ x, float *__restrict__ r,
+                                                                const float2 *__restrict__ tw1024, FusedWork w) {
+  constexpr int L = 1024, Q = L / 2 + 1, RS = 9;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] row pairs, later [8][32][33] float2
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const int row0 = blockIdx.x * 16;
+  const int rows = min(16, N - row0);
+  // stage T1[q][row0 .. row0 + 16) asynchronously; rows beyond N are zero
+  const float2 *T1s = T1 + (size_t)b * Q * N + row0;
+  for (int i = threadIdx.x; i < Q * 8; i += blockDim.x) {
+    const int q = i >> 3, pr = i & 7, rp = 2 * pr;
+    float4 *dst = st + q * RS + pr;
+    const float2 *src = T1s + (size_t)q * N + rp;
+    if (rp + 1 < rows) {
+      if (!(N & 1)) {
+        cp_async16_g(dst, src);  // N even: (q, even row) pairs are 16-byte aligned
+      } else {
+        cp_async8_g(dst, src);
+        cp_async8_g(reinterpret_cast<float2 *>(dst) + 1, src + 1);
+      }
+    } else if (rp < rows) {
+      cp_async8_g(dst, src);
+      reinterpret_cast<float2 *>(dst)[1] = float2{0.f, 0.f};
+    } else {
+      *dst = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  // scalars of slice b (overlap the staging)
+  double rho;
+  if (MODE == 0) {
+    rho = w.rho[(size_t)b * w.rho_stride + k];
+  } else {
+    rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+  }
+  double alpha;
+  if (MODE == 2) {
+    alpha = *w.tau;
+  } else {
+    const double gam = cta_reduce_parts(w.gpart + (size_t)b * gparts, gparts, red);
+    const bool bad = rho > 0 && !(gam > 0);
+    const bool frozen = bad || (w.flags && w.flags[b]);
+    alpha = (rho > 0 && !frozen) ? rho / gam : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
+  const float al = (float)alpha;
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // row pair (2 warp, 2 warp + 1): Z[q] = X_a[q] + i X_b[q], Z[L - q] = conj X_a[q] + i conj X_b[q]
+  float2 v[32];
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) {
+    const int q = lane + 32 * rr;
+    if (rr < 16 || (rr == 16 && lane == 0)) {  // q <= 512: direct
+      float4 e = st[q * RS + warp];
+      if (q == 0 || q == L / 2) { e.y = 0.f; e.w = 0.f; }  // DC / Nyquist of real rows
+      v[rr] = float2{e.x - e.w, e.y + e.z};
+    } else {
+      const float4 e = st[(L - q) * RS + warp];
+      v[rr] = float2{e.x + e.w, e.z - e.y};
+    }
+  }
+  // this warp's r (x) rows into registers: latency overlaps the FFT below
+  const int ra = row0 + 2 * warp;
+  const bool ha = ra < N, hb = ra + 1 < N;
+  float *r0 = r + ((size_t)b * N + ra) * N, *x0 = x + ((size_t)b * N + ra) * N;
+  float rv[2][16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int n = lane + 32 * m;
+    rv[0][m] = (ha && n < N) ? r0[n] : 0.f;
+    rv[1][m] = (hb && n < N) ? r0[N + n] : 0.f;
+  }
+  __syncthreads();  // staging area becomes the transpose buffers
+  float2 *tr = reinterpret_cast<float2 *>(smem_raw) + warp * (32 * 33);
+  dft32<true>(v);  // over rr: v[a] = U[lane][a]
+#pragma unroll
+  for (int a = 1; a < 32; ++a) v[a] = cmulc(v[a], __ldg(tw1024 + a * 32 + lane));
+  warp_transpose32(v, tr, lane);  // lane a: v[j] = U[j][a]
+  dft32<true>(v);                 // v[m] = z[lane + 32 m] = y_a + i y_b
+  // streaming phase: r -= alpha (G d) (and x += alpha r for SD / Landweber)
+  float ac = 0.f;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int n = lane + 32 * m;
+    if (n < N) {
+      if (ha) {
+        if (MODE != 0) x0[n] = fmaf(al, rv[0][m], x0[n]);
+        const float t = fmaf(-al, v[m].x, rv[0][m]);
+        r0[n] = t;
+        ac = fmaf(t, t, ac);
+      }
+      if (hb) {
+        if (MODE != 0) x0[N + n] = fmaf(al, rv[1][m], x0[N + n]);
+        const float t = fmaf(-al, v[m].y, rv[1][m]);
+        r0[N + n] = t;
+        ac = fmaf(t, t, ac);
+      }
+    }
+  }
+  const double s = cta_sum((double)ac, red);
+  if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
+}
+
 // ---------------------------------------------------------------- final: rho_K, resid, CG x update
 template <typename T>
 __global__ void __launch_bounds__(256) cg_final_kernel(long n, int K, int cg, T *__restrict__ x,
@@ -311,6 +446,11 @@ static bool can_vec(int N, const void *a, const void *b, const void *c) {
   return N % VW == 0 && al(a) && al(b) && al(c);
 }
 
+bool pass_c_warp_enabled() {
+  const char *e = getenv("BSCT_PASSC_V1");  // read per call: tests switch it within one process
+  return !(e && e[0] == '1');
+}
+
 template <typename T, int L, int VW>
 static cudaError_t cg_pass_a_LV(int N, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
                                 FusedWork w, cudaStream_t s) {
@@ -337,9 +477,22 @@ static cudaError_t cg_pass_c_LMV(int N, int B, int k, int gparts, const cplx<T> 
                                                                                          tw, w);
   return cudaGetLastError();
 }
+const float2 *tw1024_table();  // normal.cu
+
 template <typename T, int L, int MODE>
 static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *T1, T *x, T *r, const cplx<T> *tw,
                                 FusedWork w, cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value && L == 1024) {
+    if (pass_c_warp_enabled()) {
+      const float2 *twl = tw1024_table();
+      if (!twl) return cudaErrorMemoryAllocation;
+      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 9;
+      cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<MODE>, sm);
+      if (e != cudaSuccess) return e;
+      cg_pass_c_1024_kernel<MODE><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, gparts, T1, x, r, twl, w);
+      return cudaGetLastError();
+    }
+  }
   if (can_vec<T>(N, x, r, nullptr)) return cg_pass_c_LMV<T, L, MODE, 16 / sizeof(T)>(N, B, k, gparts, T1, x, r, tw, w, s);
   return cg_pass_c_LMV<T, L, MODE, 1>(N, B, k, gparts, T1, x, r, tw, w, s);
 }

@@ -1,0 +1,98 @@
+// fft32.cuh -- warp-level length-1024 FFT for the K5 normal operator, FP32.
+//
+// One warp computes one length-1024 DFT as a 32 x 32 four-step transform:
+//   x[t + 32 r] (lane t, register r) --DFT_32 over r--> * W_1024^{t j} --smem transpose-->
+//   (lane j, register t) --DFT_32 over t--> X[j + 32 k] (lane j, register k),
+// i.e. natural order in and out in the same lane-strided layout, one shared-memory
+// exchange per transform (row stride 33 slots: conflict-free 8-byte accesses per half
+// warp) and no block-wide barrier.  The in-register DFT_32 is radix-2 decimation in
+// frequency with compile-time twiddles followed by a compile-time bit reversal; inputs a
+// caller sets to literal zeros are folded away by the compiler, and outputs it never
+// reads are dead code (the zero-padded inputs and cropped outputs of the Toeplitz embedding).
+#pragma once
+
+#include "common.cuh"
+
+namespace bsct {
+
+__host__ __device__ constexpr double cos32(int m) {
+  m &= 31;
+  if (m > 16) m = 32 - m;  // cos is even
+  return m == 0    ? 1.0
+         : m == 1  ? 0.98078528040323044913
+         : m == 2  ? 0.92387953251128675613
+         : m == 3  ? 0.83146961230254523708
+         : m == 4  ? 0.70710678118654752440
+         : m == 5  ? 0.55557023301960222474
+         : m == 6  ? 0.38268343236508977173
+         : m == 7  ? 0.19509032201612826785
+         : m == 8  ? 0.0
+         : m == 9  ? -0.19509032201612826785
+         : m == 10 ? -0.38268343236508977173
+         : m == 11 ? -0.55557023301960222474
+         : m == 12 ? -0.70710678118654752440
+         : m == 13 ? -0.83146961230254523708
+         : m == 14 ? -0.92387953251128675613
+         : m == 15 ? -0.98078528040323044913
+                   : -1.0;
+}
+__host__ __device__ constexpr double sin32(int m) { return cos32(m - 8); }
+
+// v * exp(-+ 2 pi i m / 32) (forward: minus sign); m is a compile-time constant after unrolling
+template <bool INV>
+__device__ __forceinline__ float2 twiddle32(float2 v, int m) {
+  m &= 31;
+  if (m == 0) return v;
+  if (m == 16) return float2{-v.x, -v.y};
+  if (m == 8) return INV ? float2{-v.y, v.x} : float2{v.y, -v.x};
+  if (m == 24) return INV ? float2{v.y, -v.x} : float2{-v.y, v.x};
+  const float c = (float)cos32(m);
+  const float s = INV ? (float)sin32(m) : -(float)sin32(m);
+  return float2{v.x * c - v.y * s, v.x * s + v.y * c};
+}
+
+__host__ __device__ constexpr int bitrev5(int x) {
+  return ((x & 1) << 4) | ((x & 2) << 2) | (x & 4) | ((x & 8) >> 2) | ((x & 16) >> 4);
+}
+
+// In-register DFT_32: a[k] <- sum_n a[n] exp(-+2 pi i n k / 32), natural order in and out.
+// HALF_IN: a[16..31] are zero on entry (the zero-padded half of the Toeplitz embedding);
+// the first radix-2 stage then reduces to a twiddle (x + 0 cannot be folded by the
+// compiler without fast-math, so the pruning is explicit).
+template <bool INV, bool HALF_IN = false>
+__device__ __forceinline__ void dft32(float2 *a) {
+  if constexpr (HALF_IN) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) a[j + 16] = twiddle32<INV>(a[j], j);
+  }
+#pragma unroll
+  for (int len = HALF_IN ? 16 : 32; len >= 2; len >>= 1) {
+#pragma unroll
+    for (int blk = 0; blk < 32; blk += len) {
+#pragma unroll
+      for (int j = 0; j < len / 2; ++j) {
+        const float2 u = a[blk + j], w = a[blk + j + len / 2];
+        a[blk + j] = cadd(u, w);
+        a[blk + j + len / 2] = twiddle32<INV>(csub(u, w), j * (32 / len));
+      }
+    }
+  }
+  float2 o[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) o[bitrev5(i)] = a[i];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) a[i] = o[i];
+}
+
+// Warp transpose through shared memory: on entry lane l holds a[i] = M[l][i]; on exit lane l
+// holds a[i] = M[i][l].  tr: this warp's [32][33] float2 buffer.
+__device__ __forceinline__ void warp_transpose32(float2 *a, float2 *tr, int lane) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) tr[i * 33 + lane] = a[i];
+  __syncwarp();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) a[i] = tr[lane * 33 + i];
+  __syncwarp();
+}
+
+}  // namespace bsct

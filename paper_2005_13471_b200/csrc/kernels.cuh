@@ -65,7 +65,8 @@ template <typename T>
 cudaError_t pass_b(int N, int L, int B, cplx<T> *T1, const T *S, const cplx<T> *tw, double *gpart, cudaStream_t s);
 template <typename T>
 cudaError_t pass_c(int N, int L, int B, const cplx<T> *T1, T *y, const cplx<T> *tw, cudaStream_t s);
-int pass_b_blocks(int L);  // CTAs per slice of pass B (gpart row length)
+int pass_b_blocks(int L, bool fp32);  // CTAs per slice of pass B (gpart row length)
+bool pass_b_warp_enabled();           // FP32 L = 1024 warp-per-column pass B (BSCT_PASSB_V1=1: off)
 
 // K3/K4 (backproject.cu)
 template <typename T>

@@ -10,6 +10,12 @@
 // The 1/L^2 normalisation is folded into S.  <x, Gx> = sum_q w_q sum_p S|P~|^2
 // (Parseval; pad(x) is zero outside the crop) is reduced in pass B for the solvers.
 #include "fft.cuh"
+#include "fft32.cuh"
+
+#include <cmath>
+#include <cstdlib>
+#include <mutex>
+#include <type_traits>
 #include "kernels.cuh"
 
 namespace bsct {
@@ -112,6 +118,75 @@ __global__ void __launch_bounds__(FftLaunchB<L>::THREADS) pass_b_kernel(int N, c
       double s = 0;
       for (int i = 0; i < (int)(blockDim.x + 31) / 32; ++i) s += red[i];
       gpart[(size_t)b * gridDim.x + blockIdx.x] = s;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- pass B, L = 1024 (FP32)
+// One warp per column q (fft32.cuh): rows >= N of the column are zero (N <= L/2), so the
+// first DFT_32 sees 16 literal zeros, and only the N <= 512 kept rows of the inverse are
+// formed.  No block-wide barrier; PB_WARPS columns per CTA share the W_1024 table.
+constexpr int PB_WARPS = 4;
+
+__global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, float2 *__restrict__ T1,
+                                                                  const float *__restrict__ S,
+                                                                  const float2 *__restrict__ tw1024,
+                                                                  double *__restrict__ gpart) {
+  constexpr int L = 1024, Q = L / 2 + 1;
+  __shared__ float2 twl[32 * 32];            // W_1024^{j t}, [j][t] (symmetric)
+  __shared__ float2 trs[PB_WARPS][32 * 33];  // per-warp transpose buffers
+  __shared__ double red[PB_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) twl[i] = tw1024[i];
+  __syncthreads();
+  const int b = blockIdx.y;
+  const int q = blockIdx.x * PB_WARPS + warp;
+  double gam = 0.0;
+  if (q < Q) {
+    float2 *col = T1 + ((size_t)b * Q + q) * N;
+    float2 v[32];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      const int n = lane + 32 * r;
+      v[r] = n < N ? col[n] : float2{0.f, 0.f};
+    }
+    dft32<false, true>(v);  // over r (v[16..31] = 0): v[j] = sum_r x[lane + 32 r] W_32^{r j}
+#pragma unroll
+    for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twl[j * 32 + lane]);
+    float2 *tr = trs[warp];
+    warp_transpose32(v, tr, lane);  // lane j: v[t]
+    dft32<false>(v);                // v[k] = X[lane + 32 k]
+    const float *Sq = S + (size_t)q * L + lane;
+    // per-lane Parseval partials in FP32 (4 interleaved sums of 8 positive terms each:
+    // relative error <= 8 eps), combined in FP64 across lanes and CTAs
+    float g4[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+      const float sv = Sq[32 * k];
+      g4[k & 3] = fmaf(sv, fmaf(v[k].x, v[k].x, v[k].y * v[k].y), g4[k & 3]);
+      v[k] = float2{v[k].x * sv, v[k].y * sv};
+    }
+    gam = (double)(g4[0] + g4[1]) + (double)(g4[2] + g4[3]);
+    if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
+    dft32<true>(v);  // over k: v[a] = U[lane][a]
+#pragma unroll
+    for (int a = 1; a < 32; ++a) v[a] = cmulc(v[a], twl[a * 32 + lane]);
+    warp_transpose32(v, tr, lane);  // lane a: v[j] = U[j][a]
+    dft32<true>(v);                 // v[m] = z[lane + 32 m]
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int n = lane + 32 * m;
+      if (n < N) col[n] = v[m];
+    }
+  }
+  if (gpart) {  // deterministic CTA reduction
+    for (int o = 16; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o);
+    if (lane == 0) red[warp] = gam;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0;
+      for (int i = 0; i < PB_WARPS; ++i) t += red[i];
+      gpart[(size_t)b * gridDim.x + blockIdx.x] = t;
     }
   }
 }
@@ -274,8 +349,40 @@ static cudaError_t pass_a_L(int N, int B, const T *x, cplx<T> *T1, const cplx<T>
   pass_a_kernel<T, L><<<grid, FftLaunch<L>::THREADS, sm, s>>>(N, x, T1, tw);
   return cudaGetLastError();
 }
+// W_1024^{j t} for j, t < 32 ([32][32], FP32 rounded from long double), one copy per device,
+// uploaded on first use (outside any stream capture: plan creation runs pass B once).
+const float2 *tw1024_table() {
+  static float2 *tab[64] = {};
+  static std::mutex mu;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return nullptr;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!tab[dev]) {
+    float2 h[32 * 32];
+    for (int j = 0; j < 32; ++j)
+      for (int t = 0; t < 32; ++t) {
+        const long double ang = 6.283185307179586476925286766559L * (long double)((j * t) % 1024) / 1024.0L;
+        h[j * 32 + t] = float2{(float)cosl(ang), (float)-sinl(ang)};
+      }
+    float2 *d = nullptr;
+    if (cudaMalloc((void **)&d, sizeof(h)) != cudaSuccess) return nullptr;
+    if (cudaMemcpy(d, h, sizeof(h), cudaMemcpyHostToDevice) != cudaSuccess) return nullptr;
+    tab[dev] = d;
+  }
+  return tab[dev];
+}
+
 template <typename T, int L>
 static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T> *tw, double *gpart, cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value && L == 1024) {
+    const float2 *twl = tw1024_table();
+    if (!twl) return cudaErrorMemoryAllocation;
+    if (pass_b_warp_enabled()) {
+      pass_b_1024_kernel<<<dim3((L / 2 + 1 + PB_WARPS - 1) / PB_WARPS, B), PB_WARPS * 32, 0, s>>>(
+          N, T1, S, twl, gpart);
+      return cudaGetLastError();
+    }
+  }
   constexpr int G = FftLaunchB<L>::G;
   const size_t sm = (size_t)G * FftCfg<L>::SMEM * sizeof(cplx<T>);
   cudaError_t e = set_smem(pass_b_kernel<T, L>, sm);
@@ -307,7 +414,13 @@ static cudaError_t spectrum_L(int N, const T *taps, T *S, cplx<T> *work, const c
   return cudaGetLastError();
 }
 
-int pass_b_blocks(int L) {
+bool pass_b_warp_enabled() {
+  const char *e = getenv("BSCT_PASSB_V1");  // read per call: tests switch it within one process
+  return !(e && e[0] == '1');
+}
+
+int pass_b_blocks(int L, bool fp32) {
+  if (fp32 && L == 1024 && pass_b_warp_enabled()) return (1024 / 2 + 1 + PB_WARPS - 1) / PB_WARPS;  // FP32 warp kernel
   switch (L) {
     case 2: return (2 / 2 + 1 + FftLaunchB<2>::G - 1) / FftLaunchB<2>::G;
     case 4: return (4 / 2 + 1 + FftLaunchB<4>::G - 1) / FftLaunchB<4>::G;

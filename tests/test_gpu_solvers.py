@@ -123,3 +123,23 @@ def test_reconstruct_host_matches_device(cuda_lib):
     cuda_lib.cg_solve(plan, b, x, 10, "cg")
     torch.cuda.synchronize()
     assert torch.equal(x.cpu(), xh)
+
+
+@pytest.mark.parametrize("N", [257, 300, 512])
+@pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
+def test_warp_fft_passes_equal_generic(cuda_lib, N, solver, monkeypatch):
+    """FP32 L = 1024 warp-FFT passes B and C (fft32.cuh) against the generic block-FFT passes,
+    ragged N (odd N exercises the unaligned staging path), B = 2."""
+    cfg = CONFIGS[3].with_(N=N, n_angles=90, n_det=2 * N + 1, ellipse_scale=N / 64)
+    T = gram_taps(cfg.geometry())
+    b = rhs(cfg, T, B=2)
+    # FP32 CG amplifies rounding differences (R12): 5 iterations at 1e-4 as in test_cg_fp32
+    K, tl = (5, 1e-4) if solver == "cg" else (6, 1e-5)
+    xw, hw = run(cuda_lib, cfg, b, K, solver, B=2)
+    monkeypatch.setenv("BSCT_PASSB_V1", "1")
+    monkeypatch.setenv("BSCT_PASSC_V1", "1")
+    xg, hg = run(cuda_lib, cfg, b, K, solver, B=2)
+    assert rel_l2(xw, xg) < tl
+    assert rel_l2(hw, hg) < tl
+    xr, _ = {"cg": solvers.cg, "sd": solvers.sd, "landweber": solvers.landweber}[solver](T, b[1], K)
+    assert rel_l2(xw[1], xr) < 1e-4
