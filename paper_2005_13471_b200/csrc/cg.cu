@@ -21,6 +21,9 @@
 
 namespace bsct {
 
+const float2 *tw1024_table();  // normal.cu: W_1024^{jt}, [32][32]
+bool pass_c_warp_enabled();
+
 __device__ __forceinline__ double cta_sum(double v, double *red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int wid = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -166,6 +169,125 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N,
     const V zc = s2[pidx((L - q) & (L - 1))];
     T1s[(size_t)q * N + ra2] = V{(T)0.5 * (z.x + zc.x), (T)0.5 * (z.y - zc.y)};
     if (ra2 + 1 < N) T1s[(size_t)q * N + ra2 + 1] = V{(T)0.5 * (z.y + zc.y), (T)0.5 * (zc.x - z.x)};
+  }
+}
+
+// ---------------------------------------------------------------- pass A (CG), L = 1024 (FP32 warp FFTs)
+// Same contract as cg_pass_a_kernel (16 rows per CTA).  Streaming phase: x += alpha p,
+// p = r + beta p with 16-byte accesses, the new p rows kept in shared memory; each warp
+// then transforms one row pair (z = p_a + i p_b) with the pruned four-step FFT, splits
+// Z into the two rows' half spectra with lane shuffles (Z[L - q] sits in lane (32 - j) mod
+// 32, register 31 - k), and the CTA writes T1[q][row0 .. row0 + 16) through a [q][9]
+// float4 staging tile (128 contiguous bytes per q).
+template <int VW>
+__global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, float *__restrict__ x,
+                                                                const float *__restrict__ r,
+                                                                float *__restrict__ p, float2 *__restrict__ T1,
+                                                                const float2 *__restrict__ tw1024, FusedWork w) {
+  constexpr int L = 1024, Q = L / 2 + 1, RS = 9, PW = 512;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *ps = reinterpret_cast<float *>(smem_raw);    // [16][PW] new p rows
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] output staging (after the FFTs)
+  float2 *trb = reinterpret_cast<float2 *>(smem_raw); // [8][32][33] transposes
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.y;
+  const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+  double beta = 0.0, alpha_prev = 0.0;
+  if (k > 0) {
+    const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
+    beta = rho_prev > 0 ? rho / rho_prev : 0.0;
+    alpha_prev = w.alpha[b];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    w.rho[(size_t)b * w.rho_stride + k] = rho;
+    if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+  }
+  const float be = (float)beta, al = (float)alpha_prev;
+  const int row0 = blockIdx.x * 16;
+  const int rows = min(16, N - row0);
+  const size_t so = (size_t)b * N * N + (size_t)row0 * N;
+  // streaming phase (VW-wide): x += a p_old, p = r + b p_old; p rows -> ps, zero-padded to PW
+  // batches of UB items per thread: all 3 UB loads are issued before the first use
+  constexpr int ITEMS = 16 * (PW / VW), UB = 4;
+  for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * 256) {
+    float pv[UB][VW], rv[UB][VW], xv[UB][VW];
+    bool ok[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int i = i0 + u * 256;
+      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+      ok[u] = i < ITEMS && rr < rows && j < N;
+      if (ok[u]) {
+        const size_t e = so + (size_t)rr * N + j;
+        vload<float, VW>(pv[u], p + e);
+        vload<float, VW>(rv[u], r + e);
+        vload<float, VW>(xv[u], x + e);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int i = i0 + u * 256;
+      if (i >= ITEMS) break;
+      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+      if (ok[u]) {
+        const size_t e = so + (size_t)rr * N + j;
+#pragma unroll
+        for (int c = 0; c < VW; ++c) {
+          xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
+          pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+        }
+        vstore<float, VW>(x + e, xv[u]);
+        vstore<float, VW>(p + e, pv[u]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
+      }
+      vstore<float, VW>(ps + rr * PW + j, pv[u]);
+    }
+  }
+  __syncthreads();
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = float2{ps[(2 * warp) * PW + lane + 32 * m], ps[(2 * warp + 1) * PW + lane + 32 * m]};
+  __syncthreads();  // ps becomes the transpose buffers
+  dft32<false, true>(v);  // over m (v[16..31] = 0): v[j] = sum_m z[lane + 32 m] W_32^{m j}
+#pragma unroll
+  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], __ldg(tw1024 + j * 32 + lane));
+  float2 *tr = trb + warp * (32 * 33);
+  warp_transpose32(v, tr, lane);  // lane j: v[t]
+  dft32<false>(v);                // v[kk] = Z[lane + 32 kk]
+  __syncthreads();  // transposes done CTA-wide: the area becomes the output staging tile
+  const int src = (32 - lane) & 31;
+#pragma unroll
+  for (int kk = 0; kk <= 16; ++kk) {
+    // Z[L - q] for q = lane + 32 kk: lane (32 - lane) mod 32, register 31 - kk (lane 0: (32 - kk) mod 32)
+    float2 zc;
+    zc.x = __shfl_sync(0xffffffffu, v[kk < 16 ? 31 - kk : 15].x, src);  // kk = 16: lane 0 only
+    zc.y = __shfl_sync(0xffffffffu, v[kk < 16 ? 31 - kk : 15].y, src);
+    if (lane == 0) zc = v[(32 - kk) & 31];
+    if (kk == 16 && lane != 0) break;
+    const float2 z = v[kk];
+    const int q = lane + 32 * kk;
+    st[q * RS + warp] = make_float4(0.5f * (z.x + zc.x), 0.5f * (z.y - zc.y), 0.5f * (z.y + zc.y), 0.5f * (zc.x - z.x));
+  }
+  __syncthreads();
+  float2 *T1s = T1 + (size_t)b * Q * N + row0;
+  for (int i = threadIdx.x; i < Q * 8; i += blockDim.x) {
+    const int q = i >> 3, pr = i & 7, rp = 2 * pr;
+    if (rp >= rows) continue;
+    const float4 e = st[q * RS + pr];
+    float2 *dst = T1s + (size_t)q * N + rp;
+    if (rp + 1 < rows) {
+      if (!(N & 1)) {
+        *reinterpret_cast<float4 *>(dst) = e;
+      } else {
+        dst[0] = float2{e.x, e.y};
+        dst[1] = float2{e.z, e.w};
+      }
+    } else {
+      dst[0] = float2{e.x, e.y};
+    }
   }
 }
 
@@ -463,6 +585,23 @@ static cudaError_t cg_pass_a_LV(int N, int B, int k, T *x, const T *r, T *p, cpl
 template <typename T, int L>
 static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
                                FusedWork w, cudaStream_t s) {
+  if constexpr (std::is_same<T, float>::value && L == 1024) {
+    if (pass_c_warp_enabled()) {
+      const float2 *twl = tw1024_table();
+      if (!twl) return cudaErrorMemoryAllocation;
+      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 9;
+      if (can_vec<T>(N, x, r, p)) {
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4>, sm);
+        if (e != cudaSuccess) return e;
+        cg_pass_a_1024_kernel<4><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+      } else {
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1>, sm);
+        if (e != cudaSuccess) return e;
+        cg_pass_a_1024_kernel<1><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+      }
+      return cudaGetLastError();
+    }
+  }
   if (can_vec<T>(N, x, r, p)) return cg_pass_a_LV<T, L, 16 / sizeof(T)>(N, B, k, x, r, p, T1, tw, w, s);
   return cg_pass_a_LV<T, L, 1>(N, B, k, x, r, p, T1, tw, w, s);
 }
@@ -477,8 +616,6 @@ static cudaError_t cg_pass_c_LMV(int N, int B, int k, int gparts, const cplx<T> 
                                                                                          tw, w);
   return cudaGetLastError();
 }
-const float2 *tw1024_table();  // normal.cu
-
 template <typename T, int L, int MODE>
 static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *T1, T *x, T *r, const cplx<T> *tw,
                                 FusedWork w, cudaStream_t s) {
