@@ -156,10 +156,24 @@ bsct_status bsct_cg_solve(bsct_plan plan, const void *b, void *x, int32_t B, int
 bsct_status bsct_forward_project(bsct_plan plan, const void *c, void *sino, int32_t B, bsct_stream stream);
 
 /*
+ * Reconstruction from DEVICE buffers: x = solver^iters(G, H^T g^) per slice (one back
+ * projection, then the filter in every iteration), i.e. bsct_backproject followed by
+ * bsct_cg_solve with the same arguments, results identical to that sequence (slices may be
+ * processed in chunks of BSCT_PIPE_CHUNK slices; BSCT_PIPE_OVERLAP=1 runs the back projection
+ * of chunk c+1 on a plan-owned stream while chunk c iterates -- measured no faster on B200).
+ * sino [B][n_angles][n_det] -> x [B][N][N], stream-ordered on `stream`;
+ * resid_hist / flags as in bsct_cg_solve (may be NULL).  Uses plan workspace for b.
+ */
+bsct_status bsct_reconstruct(bsct_plan plan, const void *sino, void *x, int32_t B, int32_t iters, int32_t solver,
+                             double *resid_hist, int32_t *flags, bsct_stream stream);
+
+/*
  * End-to-end reconstruction from HOST buffers (the e2e path): copies sino_host
  * [B][n_angles][n_det] to the device, back projects, runs `iters` iterations of
  * `solver`, copies x to x_host [B][N][N], and synchronises `stream`.  Host
- * buffers should be pinned for full PCIe bandwidth.  B <= max_batch.
+ * buffers should be pinned for full PCIe bandwidth.  B <= max_batch.  Pipelined by slice
+ * chunks (BSCT_PIPE_CHUNK, default 256): each chunk's H2D copy runs on a plan-owned stream
+ * ahead of its back projection and its D2H copy after its solve, overlapping the kernels.
  */
 bsct_status bsct_reconstruct_host(bsct_plan plan, const void *sino_host, void *x_host, int32_t B, int32_t iters,
                                   int32_t solver, bsct_stream stream);

@@ -34,7 +34,7 @@ H_CORR = 25
 # exported symbols of include/bsct.h (checked by tests/test_abi.py)
 SYMBOLS = ("bsct_version", "bsct_last_error", "bsct_fft_size", "bsct_gram_build", "bsct_plan_create",
            "bsct_plan_destroy", "bsct_plan_set_filter", "bsct_plan_spectrum", "bsct_correction_filter", "bsct_backproject",
-           "bsct_normal_apply", "bsct_cg_solve", "bsct_forward_project", "bsct_reconstruct_host",
+           "bsct_normal_apply", "bsct_cg_solve", "bsct_forward_project", "bsct_reconstruct", "bsct_reconstruct_host",
            "bsct_plan_launch_count", "bsct_plan_profile", "bsct_plan_profile_read")
 
 # bsct_kernel_class
@@ -82,6 +82,7 @@ def load(path: str | None = None):
         "bsct_normal_apply": (i32, [vp, vp, vp, i32, vp]),
         "bsct_cg_solve": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "bsct_forward_project": (i32, [vp, vp, vp, i32, vp]),
+        "bsct_reconstruct": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "bsct_reconstruct_host": (i32, [vp, vp, vp, i32, i32, i32, vp]),
         "bsct_plan_launch_count": (i64, [vp]),
         "bsct_plan_profile": (i32, [vp, i32]),
@@ -262,6 +263,19 @@ def cg_solve(plan: Plan, b, x, iters: int, solver="cg", resid_hist=None, flags=N
                                 _ptr(x, plan.dtype, B * plan.N * plan.N, "x"), B, int(iters), sv,
                                 _ptr(resid_hist, torch.float64, B * iters, "resid_hist"),
                                 _ptr(flags, torch.int32, B, "flags"), _stream(stream)))
+    return x
+
+
+def reconstruct(plan: Plan, sino, x, iters: int, solver="cg", resid_hist=None, flags=None, stream=None):
+    """x[B,N,N] <- back projection of sino[B,n_angles,n_det], then `iters` solver iterations
+    (device tensors; slice chunks pipelined inside the library)."""
+    import torch
+    B = _batch(sino, plan.n_angles * plan.n_det, "sino")
+    sv = SOLVERS[solver] if isinstance(solver, str) else int(solver)
+    _check(load().bsct_reconstruct(plan.handle, _ptr(sino, plan.dtype, name="sino"),
+                                   _ptr(x, plan.dtype, B * plan.N * plan.N, "x"), B, int(iters), sv,
+                                   _ptr(resid_hist, torch.float64, B * iters, "resid_hist"),
+                                   _ptr(flags, torch.int32, B, "flags"), _stream(stream)))
     return x
 
 

@@ -86,6 +86,9 @@ struct bsct_plan_s {
   int rho_iters = -1;
   int *flags = nullptr;
   int64_t launches = 0;
+  // reconstruct pipeline: aux streams (BP / H2D, D2H) and per-chunk events
+  cudaStream_t aux = nullptr, aux2 = nullptr, hi = nullptr;  // hi: solves, highest priority
+  std::vector<cudaEvent_t> pipe_ev;
   // kernel-class profiler: CUDA events bracket every launch on the caller's stream
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_pool;
@@ -491,6 +494,10 @@ bsct_status bsct_plan_destroy(bsct_plan p) {
   for (void *b : bufs)
     if (b) cudaFree(b);
   for (cudaEvent_t e : p->prof_pool) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->pipe_ev) cudaEventDestroy(e);
+  if (p->aux) cudaStreamDestroy(p->aux);
+  if (p->aux2) cudaStreamDestroy(p->aux2);
+  if (p->hi) cudaStreamDestroy(p->hi);
   delete p;
   return BSCT_OK;
 }
@@ -613,26 +620,156 @@ bsct_status bsct_forward_project(bsct_plan p, const void *c, void *sino, int32_t
                            : forward_t<float>(p, (const float *)c, (float *)sino, B, s);
 }
 
+}  // extern "C"
+
+namespace {
+
+int pipe_chunk(int B, bool host) {
+  // host path: chunks overlap the PCIe copies with compute (measured e2e 132K -> 142K
+  // slice-iterations/s on config 5); device path: one chunk unless BSCT_PIPE_CHUNK is set
+  int c = host ? 256 : 0;
+  if (const char *e = getenv("BSCT_PIPE_CHUNK")) c = atoi(e);
+  if (c <= 0 || c >= B) return B;  // one chunk: no pipelining
+  return c;
+}
+
+bsct_status pipe_resources(bsct_plan p, int nchunks) {
+  if (!p->aux) CU(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+  if (!p->aux2) CU(cudaStreamCreateWithFlags(&p->aux2, cudaStreamNonBlocking));
+  if (!p->hi) {
+    int lo = 0, hiP = 0;
+    CU(cudaDeviceGetStreamPriorityRange(&lo, &hiP));
+    CU(cudaStreamCreateWithPriority(&p->hi, cudaStreamNonBlocking, hiP));
+  }
+  while ((int)p->pipe_ev.size() < 3 * nchunks + 3) {
+    cudaEvent_t e;
+    CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->pipe_ev.push_back(e);
+  }
+  if (!p->b_dev) CU(cudaMalloc(&p->b_dev, p->esize() * (size_t)p->N * p->N * p->max_batch));
+  return BSCT_OK;
+}
+
+// Chunked back projection -> solve.  Host buffers (non-null): chunk c's H2D copy runs on
+// aux ahead of its back projection and its D2H copy on aux2 after its solve, so the PCIe
+// transfers overlap the kernels.  Kernels run in order on the caller's stream, unless
+// BSCT_PIPE_OVERLAP=1: back projections on aux and solves on the plan's highest-priority
+// stream (measured 1-3% slower on config 5: K4 and the FFT passes contend for the same SM
+// resources, so overlapping them buys nothing; kept for experiments).
+bsct_status reconstruct_pipe(bsct_plan p, const void *sino, void *x, int B, int iters, int solver, double *resid,
+                             int32_t *flags, cudaStream_t s, const void *sino_host, void *x_host) {
+  const size_t es = p->esize();
+  const size_t sino_b = es * (size_t)p->n_angles * p->M, img_b = es * (size_t)p->N * p->N;
+  const int cb = pipe_chunk(B, sino_host != nullptr);
+  const int nch = (B + cb - 1) / cb;
+  bsct_status st = pipe_resources(p, nch);
+  if (st != BSCT_OK) return st;
+  const char *oe = getenv("BSCT_PIPE_OVERLAP");
+  const bool overlap = nch > 1 && oe && oe[0] == '1';
+  cudaStream_t sb = overlap ? p->aux : s, ss = overlap ? p->hi : s;
+  char *bdev = (char *)p->b_dev;
+  int64_t launches = 0;
+  cudaEvent_t *evH = &p->pipe_ev[0], *evB = &p->pipe_ev[nch], *evS = &p->pipe_ev[2 * nch];
+  cudaEvent_t start = p->pipe_ev[3 * nch], done = p->pipe_ev[3 * nch + 1], solved = p->pipe_ev[3 * nch + 2];
+  CU(cudaEventRecord(start, s));
+  for (cudaStream_t o : {p->aux, p->aux2, p->hi}) CU(cudaStreamWaitEvent(o, start, 0));
+  if (sino_host)
+    for (int c = 0; c < nch; ++c) {
+      const int c0 = c * cb, nb = std::min(cb, B - c0);
+      CU(cudaMemcpyAsync((char *)sino + c0 * sino_b, (const char *)sino_host + c0 * sino_b, nb * sino_b,
+                         cudaMemcpyHostToDevice, p->aux));
+      CU(cudaEventRecord(evH[c], p->aux));
+    }
+  for (int c = 0; c < nch; ++c) {
+    const int c0 = c * cb, nb = std::min(cb, B - c0);
+    const char *sc = (const char *)sino + c0 * sino_b;
+    char *bc = bdev + c0 * img_b;
+    if (sino_host) CU(cudaStreamWaitEvent(sb, evH[c], 0));
+    p->launches = 0;
+    st = p->dt == BSCT_F64 ? backproject_t<double>(p, (const double *)sc, (double *)bc, nb, sb)
+                           : backproject_t<float>(p, (const float *)sc, (float *)bc, nb, sb);
+    if (st != BSCT_OK) return st;
+    launches += p->launches;
+    if (overlap) {  // the solves wait per chunk; otherwise stream order suffices
+      CU(cudaEventRecord(evB[c], sb));
+    } else {
+      p->launches = 0;
+      st = p->dt == BSCT_F64
+               ? solve_t<double>(p, (const double *)bc, (double *)((char *)x + c0 * img_b), nb, iters, solver,
+                                 resid ? resid + (size_t)c0 * iters : nullptr, flags ? flags + c0 : nullptr, ss)
+               : solve_t<float>(p, (const float *)bc, (float *)((char *)x + c0 * img_b), nb, iters, solver,
+                                resid ? resid + (size_t)c0 * iters : nullptr, flags ? flags + c0 : nullptr, ss);
+      if (st != BSCT_OK) return st;
+      launches += p->launches;
+      if (x_host) {
+        CU(cudaEventRecord(evS[c], ss));
+        CU(cudaStreamWaitEvent(p->aux2, evS[c], 0));
+        CU(cudaMemcpyAsync((char *)x_host + c0 * img_b, (const char *)x + c0 * img_b, nb * img_b,
+                           cudaMemcpyDeviceToHost, p->aux2));
+      }
+    }
+  }
+  if (overlap)
+    for (int c = 0; c < nch; ++c) {
+      const int c0 = c * cb, nb = std::min(cb, B - c0);
+      const char *bc = bdev + c0 * img_b;
+      CU(cudaStreamWaitEvent(ss, evB[c], 0));
+      p->launches = 0;
+      st = p->dt == BSCT_F64
+               ? solve_t<double>(p, (const double *)bc, (double *)((char *)x + c0 * img_b), nb, iters, solver,
+                                 resid ? resid + (size_t)c0 * iters : nullptr, flags ? flags + c0 : nullptr, ss)
+               : solve_t<float>(p, (const float *)bc, (float *)((char *)x + c0 * img_b), nb, iters, solver,
+                                resid ? resid + (size_t)c0 * iters : nullptr, flags ? flags + c0 : nullptr, ss);
+      if (st != BSCT_OK) return st;
+      launches += p->launches;
+      if (x_host) {
+        CU(cudaEventRecord(evS[c], ss));
+        CU(cudaStreamWaitEvent(p->aux2, evS[c], 0));
+        CU(cudaMemcpyAsync((char *)x_host + c0 * img_b, (const char *)x + c0 * img_b, nb * img_b,
+                           cudaMemcpyDeviceToHost, p->aux2));
+      }
+    }
+  // join every side stream back into the caller's stream
+  CU(cudaEventRecord(done, p->aux2));
+  CU(cudaStreamWaitEvent(s, done, 0));
+  CU(cudaEventRecord(solved, p->hi));
+  CU(cudaStreamWaitEvent(s, solved, 0));
+  CU(cudaEventRecord(done, p->aux));
+  CU(cudaStreamWaitEvent(s, done, 0));
+  p->launches = launches;
+  return BSCT_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+bsct_status bsct_reconstruct(bsct_plan p, const void *sino, void *x, int32_t B, int32_t iters, int32_t solver,
+                             double *resid_hist, int32_t *flags, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
+  if (solver < BSCT_CG || solver > BSCT_LANDWEBER) return fail(BSCT_EINVAL, "unknown solver %d", solver);
+  if (B == 0) return BSCT_OK;
+  if (!sino || !x) return fail(BSCT_EINVAL, "NULL buffer");
+  return reconstruct_pipe(p, sino, x, B, iters, solver, resid_hist, flags, (cudaStream_t)stream, nullptr, nullptr);
+}
+
 bsct_status bsct_reconstruct_host(bsct_plan p, const void *sino_host, void *x_host, int32_t B, int32_t iters,
                                   int32_t solver, bsct_stream stream) {
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;
+  if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
+  if (solver < BSCT_CG || solver > BSCT_LANDWEBER) return fail(BSCT_EINVAL, "unknown solver %d", solver);
   if (!sino_host || !x_host) return fail(BSCT_EINVAL, "NULL buffer");
   cudaStream_t s = (cudaStream_t)stream;
   const size_t es = p->esize();
   const size_t sino_b = es * (size_t)p->n_angles * p->M, img_b = es * (size_t)p->N * p->N;
   if (!p->sino_dev) CU(cudaMalloc(&p->sino_dev, sino_b * p->max_batch));
-  if (!p->b_dev) CU(cudaMalloc(&p->b_dev, img_b * p->max_batch));
   if (!p->x_dev) CU(cudaMalloc(&p->x_dev, img_b * p->max_batch));
-  CU(cudaMemcpyAsync(p->sino_dev, sino_host, sino_b * B, cudaMemcpyHostToDevice, s));
-  st = bsct_backproject(p, p->sino_dev, p->b_dev, B, stream);
+  st = reconstruct_pipe(p, p->sino_dev, p->x_dev, B, iters, solver, nullptr, nullptr, s, sino_host, x_host);
   if (st != BSCT_OK) return st;
-  const int64_t l0 = p->launches;
-  st = bsct_cg_solve(p, p->b_dev, p->x_dev, B, iters, solver, nullptr, nullptr, stream);
-  if (st != BSCT_OK) return st;
-  p->launches += l0;
-  CU(cudaMemcpyAsync(x_host, p->x_dev, img_b * B, cudaMemcpyDeviceToHost, s));
   CU(cudaStreamSynchronize(s));
   return BSCT_OK;
 }

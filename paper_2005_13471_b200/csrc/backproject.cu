@@ -45,28 +45,40 @@ static cudaError_t upload_q() {
   return e;
 }
 
+// One CTA per (angle, slice-group): CR_ROWS sinogram rows of the same angle (one per slice)
+// staged in shared memory with the taps; each output sample is a 51-tap dot product with
+// the taps read from shared memory (uniform index across the warp: broadcast).  The
+// degree test is per angle, hence uniform per CTA.
+constexpr int CR_ROWS = 8;
+
 template <typename T>
-__global__ void __launch_bounds__(256) correction_kernel(int n_angles, int M, const int *__restrict__ degree,
+__global__ void __launch_bounds__(256) correction_kernel(int n_angles, int M, int B, const int *__restrict__ degree,
                                                          const T *__restrict__ sino, T *__restrict__ gt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *row = reinterpret_cast<T *>(smem_raw);
-  const int a = blockIdx.x, b = blockIdx.y;
-  const T *src = sino + ((size_t)b * n_angles + a) * M;
-  T *dst = gt + ((size_t)b * n_angles + a) * (M + 2 * HC);
+  T *rows = reinterpret_cast<T *>(smem_raw);  // [CR_ROWS][M + 4 HC], zero-extended by 2 HC each side
+  __shared__ T qs[2 * HC + 1];
+  const int a = blockIdx.x, b0 = blockIdx.y * CR_ROWS;
+  const int nb = min(CR_ROWS, B - b0);
+  const int Mp = M + 4 * HC, Mt = M + 2 * HC;
   const int d = degree[a];
-  for (int i = threadIdx.x; i < M; i += blockDim.x) row[i] = src[i];
+  if (threadIdx.x < 2 * HC + 1) qs[threadIdx.x] = qtap<T>(threadIdx.x);
+  for (int i = threadIdx.x; i < nb * Mp; i += blockDim.x) {
+    const int rr = i / Mp, m = i - rr * Mp - 2 * HC;
+    rows[i] = (m >= 0 && m < M) ? sino[((size_t)(b0 + rr) * n_angles + a) * M + m] : (T)0;
+  }
   __syncthreads();
-  for (int j = threadIdx.x; j < M + 2 * HC; j += blockDim.x) {
-    const int m = j - HC;  // detector index of output sample j
+  for (int i = threadIdx.x; i < nb * Mt; i += blockDim.x) {
+    const int rr = i / Mt, j = i - rr * Mt;  // output j <-> detector index m = j - HC
+    const T *row = rows + rr * Mp + j;       // row[u] = g[j - 2 HC + u]
     T v = 0;
     if (d == 2) {
-      // g~[m] = sum_i q[i] g[m - i], zero outside [0, M)
-      const int ilo = max(-HC, m - (M - 1)), ihi = min(HC, m);
-      for (int i = ilo; i <= ihi; ++i) v = fma(qtap<T>(i + HC), row[m - i], v);
-    } else if (m >= 0 && m < M) {
-      v = row[m];
+      // g~[m] = sum_{t=0}^{2 HC} q[t - HC] g[m - (t - HC)] = sum_t qs[t] g[j - t]
+#pragma unroll
+      for (int t = 0; t <= 2 * HC; ++t) v = fma(qs[t], row[2 * HC - t], v);
+    } else {
+      v = row[HC];
     }
-    dst[j] = v;
+    gt[((size_t)(b0 + rr) * n_angles + a) * Mt + j] = v;
   }
 }
 
@@ -74,12 +86,12 @@ template <typename T>
 cudaError_t correction_filter(int n_angles, int M, int B, const int *degree, const T *sino, T *gt, cudaStream_t s) {
   cudaError_t e = upload_q();
   if (e != cudaSuccess) return e;
-  const size_t sm = sizeof(T) * (size_t)M;
+  const size_t sm = sizeof(T) * (size_t)CR_ROWS * (M + 4 * HC);
   if (sm > 48 * 1024) {
     e = cudaFuncSetAttribute(correction_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  correction_kernel<T><<<dim3(n_angles, B), 256, sm, s>>>(n_angles, M, degree, sino, gt);
+  correction_kernel<T><<<dim3(n_angles, (B + CR_ROWS - 1) / CR_ROWS), 256, sm, s>>>(n_angles, M, B, degree, sino, gt);
   return cudaGetLastError();
 }
 

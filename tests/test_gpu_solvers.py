@@ -143,3 +143,34 @@ def test_warp_fft_passes_equal_generic(cuda_lib, N, solver, monkeypatch):
     assert rel_l2(hw, hg) < tl
     xr, _ = {"cg": solvers.cg, "sd": solvers.sd, "landweber": solvers.landweber}[solver](T, b[1], K)
     assert rel_l2(xw[1], xr) < 1e-4
+
+
+@pytest.mark.parametrize("chunk,overlap", [("0", "0"), ("2", "0"), ("2", "1"), ("3", "1")])
+@pytest.mark.parametrize("solver", ["cg", "landweber"])
+def test_reconstruct_pipeline_equals_sequence(cuda_lib, chunk, overlap, solver, monkeypatch):
+    """bsct_reconstruct (slice chunks: back projection on the plan's stream overlapping the
+    solves) is bitwise identical to bsct_backproject + bsct_cg_solve; resid/flags offsets."""
+    import torch
+    from synth.sinogram import config_sinogram
+    monkeypatch.setenv("BSCT_PIPE_CHUNK", chunk)
+    monkeypatch.setenv("BSCT_PIPE_OVERLAP", overlap)
+    cfg = CONFIGS[2].with_(N=64, n_angles=60, n_det=91, ellipse_scale=1.0)
+    g = cfg.geometry()
+    B = 5
+    sino = np.stack([config_sinogram(cfg, s) for s in range(B)]).astype(np.float32)
+    plan, taps = gpu_plan(cuda_lib, g, "f32", max_batch=B)
+    sd = to_dev(sino, "f32")
+    x = torch.empty((B, 64, 64), device="cuda")
+    h = torch.empty((B, 7), dtype=torch.float64, device="cuda")
+    cuda_lib.reconstruct(plan, sd, x, 7, solver, resid_hist=h)
+    b = torch.empty_like(x)
+    cuda_lib.backproject(plan, sd, b)
+    x2 = torch.empty_like(x)
+    h2 = torch.empty_like(h)
+    cuda_lib.cg_solve(plan, b, x2, 7, solver, resid_hist=h2)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x2)
+    assert torch.equal(h, h2)
+    xh = torch.empty((B, 64, 64), dtype=torch.float32).pin_memory()
+    cuda_lib.reconstruct_host(plan, torch.from_numpy(sino).pin_memory(), xh, 7, solver)
+    assert torch.equal(xh, x.cpu())
