@@ -65,6 +65,20 @@ def load_peaks():
     return dict(hbm_gbs=6650.0, source="fallback", sm_max_mhz=1965.0)
 
 
+def ncu_traffic(kernel: str, slices: int):
+    """DRAM bytes per launch of `kernel` from the committed ncu --set full capture
+    (profiles/*/ncu_traffic.json, bytes per slice x slices of this launch), else None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")))
+    if not files:
+        return None, None
+    d = json.load(open(files[-1]))
+    k = d["kernels"].get(kernel)
+    if not k:
+        return None, None
+    return k["bytes_per_slice"] * slices, os.path.relpath(files[-1], ROOT)
+
+
 def fp32_peak_tflops(sm_mhz: float, sms: int = 148) -> float:
     """FP32 non-tensor peak: SMs x 128 FP32 lanes x 2 flop (FMA) x clock (B200_PROFILING.md:
     148 SMs, 1965 MHz max; 4 SMSPs x 32 FP32 lanes per SM)."""
@@ -324,6 +338,18 @@ def run_ours(args):
     L = plan.L
     Q = L // 2 + 1
     vox_angles = B * N * N * n_ang
+    # compulsory HBM bytes per launch of the fused CG passes: A reads p, r, x and
+    # writes x, p and T1; B reads and writes T1; C reads T1 and reads/writes r (CG mode)
+    cg_bytes = {"pass_a": B * (20 * N * N + 8 * Q * N), "pass_b": B * 16 * Q * N,
+                "pass_c": B * (8 * Q * N + 8 * N * N),
+                "solver_update": B * 4 * N * N * 6, "solver_finish": B * 4 * N * N * 3}
+    kernels = {}
+    for kk in ("pass_a", "pass_b", "pass_c"):
+        if kk in per and per[kk][1] > 0:
+            ms1 = per[kk][0] / per[kk][1]
+            gbs = cg_bytes[kk] / (ms1 / 1e3) / 1e9
+            kernels[kk] = {"ms_per_launch": ms1, "bound": "hbm", "achieved_gbs": gbs,
+                           "frac_of_measured_hbm": gbs / peaks["hbm_gbs"]}
     if dom == "backproject":
         # algorithmic FLOP per vox-angle (K4): S_eff samples x (degree-5 Horner = 5 FMA
         # + 1 FMA accumulate) x 2 flop + 2 FMA for k_theta; S_eff = mean support / lambda_y
@@ -332,18 +358,24 @@ def run_ours(args):
         ms_launch = per[dom][0] / max(per[dom][1], 1)
         ach = flops / (ms_launch / 1e3) / 1e12
         peak = fp32_peak_tflops(clk.get("sm_max_mhz") or 1965.0)
+        tb, tsrc = ncu_traffic("bp_v3_kernel", B)
         roof = {"kernel": "backproject (K4)", "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": None,
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md)"}
+                "frac": ach / peak, "traffic": tb, "traffic_source": tsrc,
+                "algorithmic_bytes": B * 4 * (n_ang * (M + 50) + N * N),
+                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md)",
+                "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6); "
+                        "K4 v3 evaluates it from per-tile tables and is shared-memory bound (ncu L1/smem 81%)"}
     else:
         # HBM-bound FFT passes: compulsory bytes of the pass per launch (K5)
-        byts = {"pass_a": B * (4 * N * N + 8 * Q * N), "pass_b": B * 16 * Q * N,
-                "pass_c": B * (8 * Q * N + 4 * N * N),
-                "solver_update": B * 4 * N * N * 6, "solver_finish": B * 4 * N * N * 3}.get(dom, 0)
+        byts = cg_bytes.get(dom, 0)
         ms_launch = per[dom][0] / max(per[dom][1], 1)
         ach = byts / (ms_launch / 1e3) / 1e9
+        kname = {"pass_a": "cg_pass_a_1024_kernel", "pass_b": "pass_b_1024_kernel",
+                 "pass_c": "cg_pass_c_1024_kernel"}.get(dom, dom)
+        tb, tsrc = ncu_traffic(kname, B)
         roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": None, "peak_source": peaks["source"]}
+                "frac": ach / peaks["hbm_gbs"], "traffic": tb, "traffic_source": tsrc,
+                "peak_source": peaks["source"]}
 
     cpu = None
     if not args.no_cpu and ws == 1:
@@ -370,6 +402,7 @@ def run_ours(args):
         "backproj_gvox_angle_s": total * N * N * n_ang / (phases[2] / 1e3) / 1e9,
         "cg_only_slice_iter_s": total * iters / (phases[3] / 1e3),
         "kernel_ms_per_step": kernel_ms,
+        "cg_pass_rooflines": kernels,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,
