@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--solver", default="cg")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cufft", action="store_true")
     ap.add_argument("--json-out", default=None)
     return ap.parse_args()
 
@@ -377,6 +378,43 @@ def run_ours(args):
                 "frac": ach / peaks["hbm_gbs"], "traffic": tb, "traffic_source": tsrc,
                 "peak_source": peaks["source"]}
 
+    # ---- side by side (comparison only, not a product path): y = G x through cuFFT
+    # (torch.fft: rfft2 of the zero-padded L x L slice, * spectrum, irfft2, crop) against
+    # bsct_normal_apply (three fused-free FFT passes) on the same 256-slice batch
+    cufft = None
+    if not args.no_cufft:
+        nb = min(256, B)
+        xs = x[:nb].contiguous()
+        yb = torch.empty_like(xs)
+        S = torch.empty((Q, L), device=dev)
+        bsct.plan_spectrum(plan, S)
+        St = (S.t() * (L * L)).contiguous()              # [L][Q]: rfft2 layout, undo the 1/L^2
+        pad = torch.zeros((nb, L, L), device=dev)
+
+        def cufft_apply():
+            pad[:, :N, :N] = xs
+            return torch.fft.irfft2(torch.fft.rfft2(pad) * St, s=(L, L))[:, :N, :N]
+
+        ref = cufft_apply()
+        bsct.normal_apply(plan, xs, yb)
+        torch.cuda.synchronize()
+        rel = float((ref - yb).norm() / ref.norm())
+        ts = {}
+        for name, fn in (("bsct_normal_apply", lambda: bsct.normal_apply(plan, xs, yb)), ("cufft", cufft_apply)):
+            for _ in range(3):
+                fn()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(10):
+                fn()
+            a1.record()
+            torch.cuda.synchronize()
+            ts[name] = a0.elapsed_time(a1) / 10
+        cufft = {"slices": nb, "bsct_normal_apply_ms": ts["bsct_normal_apply"], "cufft_ms": ts["cufft"],
+                 "speedup": ts["cufft"] / ts["bsct_normal_apply"], "rel_l2_diff": rel,
+                 "note": "comparison only: torch.fft (cuFFT) rfft2/irfft2 of the padded slice; not used by the product"}
+        del pad, St, S, yb, xs
+
     cpu = None
     if not args.no_cpu and ws == 1:
         v, det = oracle_sample(cfg, iters, bp_stride=16, cg_iters=iters)
@@ -403,6 +441,7 @@ def run_ours(args):
         "cg_only_slice_iter_s": total * iters / (phases[3] / 1e3),
         "kernel_ms_per_step": kernel_ms,
         "cg_pass_rooflines": kernels,
+        "cufft_side_by_side": cufft,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

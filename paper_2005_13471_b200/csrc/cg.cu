@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N,
 // Z into the two rows' half spectra with lane shuffles (Z[L - q] sits in lane (32 - j) mod
 // 32, register 31 - k), and the CTA writes T1[q][row0 .. row0 + 16) through a [q][9]
 // float4 staging tile (128 contiguous bytes per q).
-template <int VW>
+template <int VW, bool PLAIN>
 __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, float *__restrict__ x,
                                                                 const float *__restrict__ r,
                                                                 float *__restrict__ p, float2 *__restrict__ T1,
@@ -192,14 +192,15 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, fl
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.y;
-  const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+  // PLAIN (y = G x): p is the input x, nothing is updated
+  const double rho = PLAIN ? 0.0 : cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
   double beta = 0.0, alpha_prev = 0.0;
-  if (k > 0) {
+  if (!PLAIN && k > 0) {
     const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
     beta = rho_prev > 0 ? rho / rho_prev : 0.0;
     alpha_prev = w.alpha[b];
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
+  if (!PLAIN && blockIdx.x == 0 && threadIdx.x == 0) {
     w.rho[(size_t)b * w.rho_stride + k] = rho;
     if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
   }
@@ -221,8 +222,10 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, fl
       if (ok[u]) {
         const size_t e = so + (size_t)rr * N + j;
         vload<float, VW>(pv[u], p + e);
-        vload<float, VW>(rv[u], r + e);
-        vload<float, VW>(xv[u], x + e);
+        if (!PLAIN) {
+          vload<float, VW>(rv[u], r + e);
+          vload<float, VW>(xv[u], x + e);
+        }
       }
     }
 #pragma unroll
@@ -231,14 +234,16 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, fl
       if (i >= ITEMS) break;
       const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
       if (ok[u]) {
-        const size_t e = so + (size_t)rr * N + j;
+        if (!PLAIN) {
+          const size_t e = so + (size_t)rr * N + j;
 #pragma unroll
-        for (int c = 0; c < VW; ++c) {
-          xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
-          pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+          for (int c = 0; c < VW; ++c) {
+            xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
+            pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+          }
+          vstore<float, VW>(x + e, xv[u]);
+          vstore<float, VW>(p + e, pv[u]);
         }
-        vstore<float, VW>(x + e, xv[u]);
-        vstore<float, VW>(p + e, pv[u]);
       } else {
 #pragma unroll
         for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
@@ -427,9 +432,10 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, in
     }
   }
   asm volatile("cp.async.commit_group;\n" ::);
-  // scalars of slice b (overlap the staging)
-  double rho;
-  if (MODE == 0) {
+  // scalars of slice b (overlap the staging); MODE 3 (y = G x) has none
+  double rho = 0.0;
+  if (MODE == 3) {
+  } else if (MODE == 0) {
     rho = w.rho[(size_t)b * w.rho_stride + k];
   } else {
     rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
@@ -438,8 +444,9 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, in
       if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
     }
   }
-  double alpha;
-  if (MODE == 2) {
+  double alpha = 0.0;
+  if (MODE == 3) {
+  } else if (MODE == 2) {
     alpha = *w.tau;
   } else {
     const double gam = cta_reduce_parts(w.gpart + (size_t)b * gparts, gparts, red);
@@ -448,7 +455,7 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, in
     alpha = (rho > 0 && !frozen) ? rho / gam : 0.0;
     if (blockIdx.x == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
+  if (MODE != 3 && blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
   const float al = (float)alpha;
   asm volatile("cp.async.wait_group 0;\n" ::);
   __syncthreads();
@@ -474,8 +481,8 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, in
 #pragma unroll
   for (int m = 0; m < 16; ++m) {
     const int n = lane + 32 * m;
-    rv[0][m] = (ha && n < N) ? r0[n] : 0.f;
-    rv[1][m] = (hb && n < N) ? r0[N + n] : 0.f;
+    rv[0][m] = (MODE != 3 && ha && n < N) ? r0[n] : 0.f;
+    rv[1][m] = (MODE != 3 && hb && n < N) ? r0[N + n] : 0.f;
   }
   __syncthreads();  // staging area becomes the transpose buffers
   float2 *tr = reinterpret_cast<float2 *>(smem_raw) + warp * (32 * 33);
@@ -490,6 +497,11 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, in
   for (int m = 0; m < 16; ++m) {
     const int n = lane + 32 * m;
     if (n < N) {
+      if (MODE == 3) {  // y = G x into the r pointer
+        if (ha) r0[n] = v[m].x;
+        if (hb) r0[N + n] = v[m].y;
+        continue;
+      }
       if (ha) {
         if (MODE != 0) x0[n] = fmaf(al, rv[0][m], x0[n]);
         const float t = fmaf(-al, v[m].x, rv[0][m]);
@@ -504,6 +516,7 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, in
       }
     }
   }
+  if (MODE == 3) return;  // y = G x: no partials
   const double s = cta_sum((double)ac, red);
   if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
 }
@@ -591,13 +604,13 @@ static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx
       if (!twl) return cudaErrorMemoryAllocation;
       constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 9;
       if (can_vec<T>(N, x, r, p)) {
-        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, false>, sm);
         if (e != cudaSuccess) return e;
-        cg_pass_a_1024_kernel<4><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_1024_kernel<4, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
       } else {
-        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, false>, sm);
         if (e != cudaSuccess) return e;
-        cg_pass_a_1024_kernel<1><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_1024_kernel<1, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
       }
       return cudaGetLastError();
     }
@@ -681,6 +694,42 @@ cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork
   int vb = (int)((n + 2047) / 2048);
   vb = vb < 1 ? 1 : (vb > 128 ? 128 : vb);
   cg_final_kernel<T><<<dim3(cg ? vb : 1, B), 256, 0, s>>>(n, K, cg, x, p, w);
+  return cudaGetLastError();
+}
+
+// y = G x with the warp-FFT passes (FP32, L = 1024): pass A in PLAIN mode (x -> T1), pass B
+// (normal.cu), pass C in MODE 3 (T1 -> y).  Returns cudaErrorNotSupported otherwise.
+cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaStream_t s) {
+  if (L != 1024 || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  const float2 *twl = tw1024_table();
+  if (!twl) return cudaErrorMemoryAllocation;
+  constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * 9;
+  FusedWork w{};
+  w.nparts = fused_parts(N, L);
+  w.B = B;
+  float *xp = const_cast<float *>(x);
+  if (can_vec<float>(N, x, nullptr, nullptr)) {
+    cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, true>, sm);
+    if (e != cudaSuccess) return e;
+    cg_pass_a_1024_kernel<4, true><<<dim3(w.nparts, B), 256, sm, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
+  } else {
+    cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, true>, sm);
+    if (e != cudaSuccess) return e;
+    cg_pass_a_1024_kernel<1, true><<<dim3(w.nparts, B), 256, sm, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
+  }
+  return cudaGetLastError();
+}
+cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaStream_t s) {
+  if (L != 1024 || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  const float2 *twl = tw1024_table();
+  if (!twl) return cudaErrorMemoryAllocation;
+  constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * 9;
+  FusedWork w{};
+  w.nparts = fused_parts(N, L);
+  w.B = B;
+  cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<3>, sm);
+  if (e != cudaSuccess) return e;
+  cg_pass_c_1024_kernel<3><<<dim3(w.nparts, B), 256, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w);
   return cudaGetLastError();
 }
 

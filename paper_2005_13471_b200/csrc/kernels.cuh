@@ -67,6 +67,7 @@ template <typename T>
 cudaError_t pass_c(int N, int L, int B, const cplx<T> *T1, T *y, const cplx<T> *tw, cudaStream_t s);
 int pass_b_blocks(int L, bool fp32);  // CTAs per slice of pass B (gpart row length)
 bool pass_b_warp_enabled();           // FP32 L = 1024 warp-per-column pass B (BSCT_PASSB_V1=1: off)
+bool pass_c_warp_enabled();           // FP32 L = 1024 warp-FFT passes A and C (BSCT_PASSC_V1=1: off)
 
 // K3/K4 (backproject.cu)
 template <typename T>
@@ -134,6 +135,9 @@ struct FusedWork {
   double *tau;     // Landweber step (device)
 };
 int fused_parts(int N, int L);
+// y = G x with the FP32 L = 1024 warp-FFT passes A and C (cudaErrorNotSupported otherwise)
+cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaStream_t s);
+cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaStream_t s);
 template <typename T>
 cudaError_t fused_init(int N, int B, const T *b, T *x, T *r, T *p, FusedWork w, cudaStream_t s);
 template <typename T>
