@@ -415,6 +415,40 @@ def run_ours(args):
                  "note": "comparison only: torch.fft (cuFFT) rfft2/irfft2 of the padded slice; not used by the product"}
         del pad, St, S, yb, xs
 
+    # ---- config 4 Gram build (side measurement): the full N = 1024,
+    # 720-angle filter on one GPU, and the 8 angle shards one rank each would build before
+    # the allreduce (the shards run here back to back on one GPU; max over shards reported)
+    gram4 = None
+    if not args.no_cufft:
+        g4 = CONFIGS[4].geometry()
+        N4 = CONFIGS[4].N
+        t4 = torch.empty((2 * N4 - 1, 2 * N4 - 1), device=dev)
+        part = torch.empty_like(t4)
+
+        def timed(fn, reps=5):
+            fn()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(reps):
+                fn()
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+
+        full_ms = timed(lambda: bsct.gram_build(g4, t4))
+        na = len(g4["angles"])
+        shard_ms, acc = [], torch.zeros_like(t4)
+        for r in range(8):
+            lo, hi = r * na // 8, (r + 1) * na // 8
+            shard_ms.append(timed(lambda: bsct.gram_build(g4, part, lo, hi)))
+            acc += part
+        rel = float((acc - t4).norm() / t4.norm())
+        gram4 = {"N": N4, "n_angles": na, "full_ms": full_ms, "shard8_ms_max": max(shard_ms),
+                 "shard8_sum_rel_diff": rel,
+                 "note": "8 angle shards built back to back on one GPU (a rank's compute before the NCCL "
+                         "allreduce of the 16.8 MB partial filter, which is not measured here)"}
+        del t4, part, acc
+
     cpu = None
     if not args.no_cpu and ws == 1:
         v, det = oracle_sample(cfg, iters, bp_stride=16, cg_iters=iters)
@@ -442,6 +476,7 @@ def run_ours(args):
         "kernel_ms_per_step": kernel_ms,
         "cg_pass_rooflines": kernels,
         "cufft_side_by_side": cufft,
+        "gram_config4": gram4,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

@@ -18,8 +18,10 @@ Modules
   gram        Gram taps P:96-131; brute-force H^T H    pinned: tests/test_oracle_gram.py
   normal      Toeplitz apply (direct, FFT) P:131       pinned: tests/test_oracle_normal.py
   backproject correction filter Eq.(5), H^T g^         pinned: tests/test_oracle_backproject.py
-  forward     H c, Eq.(3)-(4); geometric footprints    pinned: tests/test_oracle_forward.py
+  forward     H c, Eq.(3)-(4); geometric footprints;   pinned: tests/test_oracle_forward.py
+              plain adjoint H^T (dot-product test)
   solvers     CG / steepest descent / Landweber        pinned: tests/test_oracle_solvers.py
+  sirt        SIRT on H / H^T (NEXT-1)                 pinned: tests/test_oracle_sirt.py
 Parity unpinned: none of the functions above (every one has an independent pin);
 the FP32 CG iterate itself is chaotic -- see DESIGN.md.
 """

@@ -46,3 +46,24 @@ def forward_geometric(geom, c: np.ndarray) -> np.ndarray:
                 if c[k1, k2] != 0.0:
                     out[it] += c[k1, k2] * footprint(y, t, (xs[k1], xs[k2]), g.lambda_x, g.zeta)
     return out
+
+
+def adjoint(geom, g: np.ndarray) -> np.ndarray:
+    """Plain adjoint of the sampled forward model: (H^T g)[k] = lambda_x^2 sum_t sum_m g[t, m]
+    M_[lambda_x|cos t|, lambda_x|sin t|, zeta](y_m - k_t) -- the transpose of `forward` (no
+    interpolation of g; contrast backproject.backproject).  Used by SIRT."""
+    g0 = as_geometry(geom)
+    y = g0.detector_positions()
+    out = np.zeros((g0.N, g0.N))
+    for it, t in enumerate(g0.angles):
+        w = g0.blurred_widths(t)
+        half = 0.5 * sum(kept_widths(w))
+        kt = g0.k_theta(t)
+        for m in range(g0.n_det):
+            if g[it, m] == 0.0:
+                continue
+            arg = y[m] - kt
+            msk = np.abs(arg) < half
+            if msk.any():
+                out[msk] += g0.lambda_x ** 2 * g[it, m] * box_spline(w, arg[msk])
+    return out
