@@ -449,6 +449,36 @@ def run_ours(args):
                          "allreduce of the 16.8 MB partial filter, which is not measured here)"}
         del t4, part, acc
 
+    # ---- NEXT-1 (side measurement): forward projector H, plain adjoint H^T and one SIRT
+    # iteration on 256 of the slices, against one filter-based CG iteration on the same slices
+    # -- the per-iteration cost the paper's method avoids (P:4)
+    next1 = None
+    if not args.no_cufft:
+        nb = min(256, B)
+        xs = x[:nb].contiguous()
+        hs = torch.empty((nb, n_ang, M), device=dev)
+        ims = torch.empty((nb, N, N), device=dev)
+
+        def tm(fn, reps=3):
+            fn()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record()
+            for _ in range(reps):
+                fn()
+            a1.record()
+            torch.cuda.synchronize()
+            return a0.elapsed_time(a1) / reps
+
+        f_ms = tm(lambda: bsct.forward_project(plan, xs, hs))
+        a_ms = tm(lambda: bsct.adjoint_project(plan, sino[:nb], ims))
+        s_ms = tm(lambda: bsct.sirt_solve(plan, sino[:nb], ims, 2)) - tm(lambda: bsct.sirt_solve(plan, sino[:nb], ims, 1))
+        c_ms = (tm(lambda: bsct.cg_solve(plan, xs, ims, 12)) - tm(lambda: bsct.cg_solve(plan, xs, ims, 2))) / 10
+        va = nb * N * N * n_ang
+        next1 = {"slices": nb, "forward_ms": f_ms, "forward_gvox_angle_s": va / (f_ms / 1e3) / 1e9,
+                 "adjoint_ms": a_ms, "adjoint_gvox_angle_s": va / (a_ms / 1e3) / 1e9,
+                 "sirt_iteration_ms": s_ms, "cg_iteration_ms": c_ms, "sirt_over_cg": s_ms / c_ms}
+        del hs, ims, xs
+
     cpu = None
     if not args.no_cpu and ws == 1:
         v, det = oracle_sample(cfg, iters, bp_stride=16, cg_iters=iters)
@@ -477,6 +507,7 @@ def run_ours(args):
         "cg_pass_rooflines": kernels,
         "cufft_side_by_side": cufft,
         "gram_config4": gram4,
+        "next1_projection_iteration": next1,
         "roofline": roof,
         "cpu_baseline": cpu,
         "e2e": e2e,

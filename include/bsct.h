@@ -156,6 +156,28 @@ bsct_status bsct_cg_solve(bsct_plan plan, const void *b, void *x, int32_t B, int
 bsct_status bsct_forward_project(bsct_plan plan, const void *c, void *sino, int32_t B, bsct_stream stream);
 
 /*
+ * Plain adjoint of the sampled forward model (SIRT's back projection; NEXT-1):
+ *     img[k] = lambda_x^2 sum_t sum_m sino[t][m] M_[l|c|, l|s|, zeta](y_m - k_t)
+ * i.e. the transpose of bsct_forward_project (no correction filter, no interpolant --
+ * contrast bsct_backproject).  sino [B][n_angles][n_det] -> img [B][N][N].
+ * Runs on the K4 kernels with the forward model's box-spline tables (built on first use).
+ * BSCT_EINVAL if the geometry is outside K4 v2/v3's support (detector step much finer
+ * than the pixel: more than 12 samples per cell).
+ */
+bsct_status bsct_adjoint_project(bsct_plan plan, const void *sino, void *img, int32_t B, bsct_stream stream);
+
+/*
+ * SIRT (simultaneous iterative reconstruction technique) on the forward model, the
+ * projection-based iteration the paper's filter method avoids (P:4):
+ *     x_0 = 0,  x_{k+1} = x_k + C H^T R (sino - H x_k),
+ *     R = 1 / (H 1) per detector sample, C = 1 / (H^T 1) per pixel (0 where the sum is 0),
+ * H = bsct_forward_project, H^T = bsct_adjoint_project.  sino [B][n_angles][n_det] ->
+ * x [B][N][N].  Weights are computed on first use and kept by the plan.
+ */
+bsct_status bsct_sirt_solve(bsct_plan plan, const void *sino, void *x, int32_t B, int32_t iters,
+                            bsct_stream stream);
+
+/*
  * Reconstruction from DEVICE buffers: x = solver^iters(G, H^T g^) per slice (one back
  * projection, then the filter in every iteration), i.e. bsct_backproject followed by
  * bsct_cg_solve with the same arguments, results identical to that sequence (slices may be

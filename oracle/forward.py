@@ -48,12 +48,27 @@ def forward_geometric(geom, c: np.ndarray) -> np.ndarray:
     return out
 
 
-def adjoint(geom, g: np.ndarray) -> np.ndarray:
+def adjoint(geom, g: np.ndarray, pixels=None) -> np.ndarray:
     """Plain adjoint of the sampled forward model: (H^T g)[k] = lambda_x^2 sum_t sum_m g[t, m]
     M_[lambda_x|cos t|, lambda_x|sin t|, zeta](y_m - k_t) -- the transpose of `forward` (no
-    interpolation of g; contrast backproject.backproject).  Used by SIRT."""
+    interpolation of g; contrast backproject.backproject).  Used by SIRT.
+    pixels=(k1, k2): only those pixels (same sum, evaluated one by one)."""
     g0 = as_geometry(geom)
     y = g0.detector_positions()
+    if pixels is not None:
+        xs = g0.pixel_centres()
+        p1, p2 = xs[np.asarray(pixels[0])], xs[np.asarray(pixels[1])]
+        out = np.zeros(len(p1))
+        for it, t in enumerate(g0.angles):
+            w = g0.blurred_widths(t)
+            half = 0.5 * sum(kept_widths(w))
+            kt = -np.sin(t) * p1 + np.cos(t) * p2
+            arg = y[:, None] - kt[None, :]                 # [M, P]
+            msk = np.abs(arg) < half
+            val = np.zeros_like(arg)
+            val[msk] = box_spline(w, arg[msk])
+            out += g0.lambda_x ** 2 * (g[it][:, None] * val).sum(axis=0)
+        return out
     out = np.zeros((g0.N, g0.N))
     for it, t in enumerate(g0.angles):
         w = g0.blurred_widths(t)

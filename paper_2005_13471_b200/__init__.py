@@ -35,6 +35,7 @@ H_CORR = 25
 SYMBOLS = ("bsct_version", "bsct_last_error", "bsct_fft_size", "bsct_gram_build", "bsct_plan_create",
            "bsct_plan_destroy", "bsct_plan_set_filter", "bsct_plan_spectrum", "bsct_correction_filter", "bsct_backproject",
            "bsct_normal_apply", "bsct_cg_solve", "bsct_forward_project", "bsct_reconstruct", "bsct_reconstruct_host",
+           "bsct_adjoint_project", "bsct_sirt_solve",
            "bsct_plan_launch_count", "bsct_plan_profile", "bsct_plan_profile_read")
 
 # bsct_kernel_class
@@ -83,6 +84,8 @@ def load(path: str | None = None):
         "bsct_cg_solve": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "bsct_forward_project": (i32, [vp, vp, vp, i32, vp]),
         "bsct_reconstruct": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
+        "bsct_adjoint_project": (i32, [vp, vp, vp, i32, vp]),
+        "bsct_sirt_solve": (i32, [vp, vp, vp, i32, i32, vp]),
         "bsct_reconstruct_host": (i32, [vp, vp, vp, i32, i32, i32, vp]),
         "bsct_plan_launch_count": (i64, [vp]),
         "bsct_plan_profile": (i32, [vp, i32]),
@@ -276,6 +279,22 @@ def reconstruct(plan: Plan, sino, x, iters: int, solver="cg", resid_hist=None, f
                                    _ptr(x, plan.dtype, B * plan.N * plan.N, "x"), B, int(iters), sv,
                                    _ptr(resid_hist, torch.float64, B * iters, "resid_hist"),
                                    _ptr(flags, torch.int32, B, "flags"), _stream(stream)))
+    return x
+
+
+def adjoint_project(plan: Plan, sino, img, stream=None):
+    """img[B,N,N] <- H^T sino (plain adjoint of forward_project; SIRT's back projection)."""
+    B = _batch(sino, plan.n_angles * plan.n_det, "sino")
+    _check(load().bsct_adjoint_project(plan.handle, _ptr(sino, plan.dtype, name="sino"),
+                                       _ptr(img, plan.dtype, B * plan.N * plan.N, "img"), B, _stream(stream)))
+    return img
+
+
+def sirt_solve(plan: Plan, sino, x, iters: int, stream=None):
+    """x[B,N,N] <- `iters` SIRT iterations on sino[B,n_angles,n_det] from x = 0."""
+    B = _batch(sino, plan.n_angles * plan.n_det, "sino")
+    _check(load().bsct_sirt_solve(plan.handle, _ptr(sino, plan.dtype, name="sino"),
+                                  _ptr(x, plan.dtype, B * plan.N * plan.N, "x"), B, int(iters), _stream(stream)))
     return x
 
 

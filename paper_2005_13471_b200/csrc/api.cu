@@ -79,6 +79,10 @@ struct bsct_plan_s {
   int bp_maxp = 9;            // K4 v2 sub-intervals per detector cell (max over angles)
   bool solver_v1 = false;     // unfused 5-launch iteration (A/B testing only)
   bool bp_v3 = true;          // FP32: K4 v3 (slices per CTA); BSCT_BP_V2=1 selects v2 (A/B testing)
+  // plain adjoint H^T and SIRT (NEXT-1): K4 tables without the interpolation widths, weights
+  BPAngle *adj_ang = nullptr;
+  void *adj_B = nullptr;
+  void *sirt_R = nullptr, *sirt_C = nullptr, *sino_tmp = nullptr;
   void *T1 = nullptr, *gt = nullptr, *r = nullptr, *p = nullptr, *q = nullptr;
   void *sino_dev = nullptr, *b_dev = nullptr, *x_dev = nullptr;  // reconstruct_host staging
   double *alpha = nullptr, *gpart = nullptr, *rpart = nullptr, *tau = nullptr;
@@ -242,7 +246,7 @@ bsct_status plan_filter_t(bsct_plan p, const void *taps, cudaStream_t s) {
   LAUNCH(p, BSCT_K_TABLES, 1, (build_pp_tables<T>(p->angles, n, PP_FWD, p->lx, p->ly, p->zeta, fw, s)));
   if (p->bp_cells > 0)
     LAUNCH(p, BSCT_K_TABLES, 1,
-           (build_bp_tables<T>(N, p->M, p->lx, p->ly, p->zeta, n, bp, p->bp_ang, (T *)p->bp_B, s)));
+           (build_bp_tables<T>(N, p->M, p->lx, p->ly, p->zeta, n, bp, p->bp_ang, (T *)p->bp_B, s, 1)));
   LAUNCH(p, BSCT_K_SPECTRUM, 2,
          (filter_spectrum<T>(N, L, (const T *)taps, (T *)p->S, (cplx<T> *)p->spec_work, (const cplx<T> *)p->tw, s)));
   LAUNCH(p, BSCT_K_SPECTRUM, 2, (spectrum_max<T>(L, (const T *)p->S, p->tau, s)));
@@ -435,11 +439,117 @@ bsct_status forward_t(bsct_plan p, const T *c, T *sino, int B, cudaStream_t s) {
   return BSCT_OK;
 }
 
+// ---- NEXT-1: plain adjoint H^T (K4 machinery with the forward model's kernel) and SIRT
+template <typename T>
+bsct_status adjoint_core(bsct_plan p, const T *gt, T *out, int B, cudaStream_t s) {
+  const double scale = p->lx * p->lx;  // H[(t,m), k] = lambda_x^2 M_[l|c|, l|s|, zeta](y_m - k_t)
+  const int sb = (std::is_same<T, float>::value && p->bp_v3) ? bp_v3_slices(B, p->bp_maxp, p->bp_cells) : 0;
+  if (sb > 0)
+    LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+           (backproject_v3(p->N, p->n_angles, p->M, B, p->adj_ang, (const float *)p->adj_B, (const float *)gt,
+                           (float *)out, p->bp_cells, p->bp_maxp, scale, sb, s)));
+  else
+    LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+           (backproject_v2<T>(p->N, p->n_angles, p->M, B, p->adj_ang, (const T *)p->adj_B, gt, out, p->bp_cells,
+                              p->bp_maxp, scale, s)));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status adjoint_tables(bsct_plan p, cudaStream_t s) {
+  if (p->adj_ang) return BSCT_OK;
+  if (p->bp_cells <= 0) return fail(BSCT_EINVAL, "adjoint/SIRT need a geometry supported by K4 v2/v3");
+  CU(cudaMalloc((void **)&p->adj_ang, sizeof(BPAngle) * p->n_angles));
+  CU(cudaMalloc(&p->adj_B, sizeof(T) * bp_table_floats(p->n_angles)));
+  PPTables<T> bp = tables_of<T>(p->bp_mem, p->n_angles);
+  LAUNCH(p, BSCT_K_TABLES, 1,
+         (build_bp_tables<T>(p->N, p->M, p->lx, p->ly, p->zeta, p->n_angles, bp, p->adj_ang, (T *)p->adj_B, s, 0)));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status adjoint_t(bsct_plan p, const T *sino, T *out, int B, cudaStream_t s) {
+  bsct_status st = adjoint_tables<T>(p, s);
+  if (st != BSCT_OK) return st;
+  LAUNCH(p, BSCT_K_CORRECTION, 1, (pad_rows<T>(p->n_angles, p->M, B, sino, nullptr, nullptr, (T *)p->gt, s)));
+  return adjoint_core<T>(p, (const T *)p->gt, out, B, s);
+}
+
+template <typename T>
+bsct_status sirt_weights(bsct_plan p, cudaStream_t s) {
+  if (p->sirt_R) return BSCT_OK;
+  const size_t ns = (size_t)p->n_angles * p->M, nn = (size_t)p->N * p->N;
+  CU(cudaMalloc(&p->sirt_R, sizeof(T) * ns));
+  CU(cudaMalloc(&p->sirt_C, sizeof(T) * nn));
+  T *ones_img = nullptr, *ones_sino = nullptr;
+  CU(cudaMallocAsync((void **)&ones_img, sizeof(T) * nn, s));
+  CU(cudaMallocAsync((void **)&ones_sino, sizeof(T) * ns, s));
+  std::vector<T> h1(std::max(ns, nn), (T)1);
+  CU(cudaMemcpyAsync(ones_img, h1.data(), sizeof(T) * nn, cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(ones_sino, h1.data(), sizeof(T) * ns, cudaMemcpyHostToDevice, s));
+  bsct_status st = forward_t<T>(p, ones_img, (T *)p->sirt_R, 1, s);  // row sums H 1
+  if (st == BSCT_OK) st = adjoint_t<T>(p, ones_sino, (T *)p->sirt_C, 1, s);  // column sums H^T 1
+  if (st != BSCT_OK) return st;
+  CU(safe_reciprocal<T>((long)ns, (T *)p->sirt_R, s));
+  CU(safe_reciprocal<T>((long)nn, (T *)p->sirt_C, s));
+  CU(cudaStreamSynchronize(s));  // h1 is a host temporary
+  CU(cudaFreeAsync(ones_img, s));
+  CU(cudaFreeAsync(ones_sino, s));
+  return BSCT_OK;
+}
+
+// x_{k+1} = x_k + C H^T R (g - H x_k), x_0 = 0 (oracle/sirt.py)
+template <typename T>
+bsct_status sirt_t(bsct_plan p, const T *sino, T *x, int B, int iters, cudaStream_t s) {
+  bsct_status st = adjoint_tables<T>(p, s);
+  if (st == BSCT_OK) st = sirt_weights<T>(p, s);
+  if (st != BSCT_OK) return st;
+  const size_t ns = (size_t)p->n_angles * p->M, nn = (size_t)p->N * p->N;
+  if (!p->sino_tmp) CU(cudaMalloc(&p->sino_tmp, sizeof(T) * ns * p->max_batch));
+  CU(cudaMemsetAsync(x, 0, sizeof(T) * nn * B, s));
+  for (int it = 0; it < iters; ++it) {
+    if (it > 0) {
+      st = forward_t<T>(p, x, (T *)p->sino_tmp, B, s);
+      if (st != BSCT_OK) return st;
+    }
+    LAUNCH(p, BSCT_K_CORRECTION, 1,
+           (pad_rows<T>(p->n_angles, p->M, B, sino, it > 0 ? (const T *)p->sino_tmp : nullptr,
+                        (const T *)p->sirt_R, (T *)p->gt, s)));
+    st = adjoint_core<T>(p, (const T *)p->gt, (T *)p->q, B, s);
+    if (st != BSCT_OK) return st;
+    LAUNCH(p, BSCT_K_SOLVER_UPDATE, 1, (sirt_update<T>((long)nn, B, (const T *)p->sirt_C, (const T *)p->q, x, s)));
+  }
+  return BSCT_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int32_t bsct_version(void) { return 100; }
+
+bsct_status bsct_adjoint_project(bsct_plan p, const void *sino, void *img, int32_t B, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (B == 0) return BSCT_OK;
+  if (!sino || !img) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? adjoint_t<double>(p, (const double *)sino, (double *)img, B, s)
+                           : adjoint_t<float>(p, (const float *)sino, (float *)img, B, s);
+}
+
+bsct_status bsct_sirt_solve(bsct_plan p, const void *sino, void *x, int32_t B, int32_t iters, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
+  if (B == 0) return BSCT_OK;
+  if (!sino || !x) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? sirt_t<double>(p, (const double *)sino, (double *)x, B, iters, s)
+                           : sirt_t<float>(p, (const float *)sino, (float *)x, B, iters, s);
+}
 
 const char *bsct_last_error(void) { return g_err.c_str(); }
 
@@ -496,7 +606,8 @@ bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *
 
 bsct_status bsct_plan_destroy(bsct_plan p) {
   if (!p) return BSCT_OK;
-  void *bufs[] = {p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->r, p->p, p->q,
+  void *bufs[] = {p->adj_ang, p->adj_B, p->sirt_R, p->sirt_C, p->sino_tmp,
+                  p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->r, p->p, p->q,
                   p->sino_dev, p->b_dev, p->x_dev, p->spec_work, p->bp_ang, p->bp_B, p->alpha, p->gpart, p->rpart, p->tau, p->rho, p->flags};
   for (void *b : bufs)
     if (b) cudaFree(b);

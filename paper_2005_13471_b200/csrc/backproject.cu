@@ -150,10 +150,13 @@ cudaError_t backproject(int N, double lx, double ly, int n_angles, int M, int B,
 
 size_t bp_table_floats(int n) { return (size_t)n * BP_PMAX * BP_SMAX * 8; }
 
+// interp = 1: the back projection's kernel C_t = [l|c|, l|s|, zeta] U [lambda_y]^(d+1) (degree-d
+// B-spline interpolant of g); interp = 0: the plain adjoint of the sampled forward
+// model, C_t = M_[l|c|, l|s|, zeta] (H^T, used by SIRT).  Same breakpoint structure.
 template <typename T>
 __global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx, double ly, double zeta, int n,
                                                         const double *__restrict__ cs, const int *__restrict__ degree,
-                                                        BPAngle *__restrict__ ang, T *__restrict__ Btab) {
+                                                        BPAngle *__restrict__ ang, T *__restrict__ Btab, int interp) {
   const int a = blockIdx.x;
   const int tid = threadIdx.x;
   __shared__ double w[8], sig[64], bp[16], wb[4];
@@ -169,7 +172,8 @@ __global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx,
     if (zeta > 0) raw[nr++] = zeta;
     const int d = degree[a];
     const int nbr = nr;
-    for (int i = 0; i <= d; ++i) raw[nr++] = ly;
+    if (interp)
+      for (int i = 0; i <= d; ++i) raw[nr++] = ly;
     double ssum = 0;
     for (int i = 0; i < nr; ++i) ssum += raw[i];
     const double thr = 1e-12 * fmax(1.0, ssum);
@@ -271,10 +275,43 @@ __global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx,
 
 template <typename T>
 cudaError_t build_bp_tables(int N, int M, double lx, double ly, double zeta, int n, const PPTables<T> &tb,
-                            BPAngle *ang, T *Btab, cudaStream_t s) {
-  bp_tables_kernel<T><<<n, 128, 0, s>>>(N, M, lx, ly, zeta, n, tb.cs, tb.degree, ang, Btab);
+                            BPAngle *ang, T *Btab, cudaStream_t s, int interp) {
+  bp_tables_kernel<T><<<n, 128, 0, s>>>(N, M, lx, ly, zeta, n, tb.cs, tb.degree, ang, Btab, interp);
   return cudaGetLastError();
 }
+
+// gt[b][a][j] = w[a][m] (g[b][a][m] - h[b][a][m]) for m = j - HC in [0, M), zero in the HC-wide
+// ends (the layout K4 reads); w and h may be null (factor 1, nothing subtracted).
+template <typename T>
+__global__ void __launch_bounds__(256) pad_rows_kernel(int n_angles, int M, int B, const T *__restrict__ g,
+                                                       const T *__restrict__ h, const T *__restrict__ w,
+                                                       T *__restrict__ gt) {
+  const int Mt = M + 2 * HC;
+  const size_t total = (size_t)B * n_angles * Mt;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t row = i / Mt;
+    const int m = (int)(i - row * Mt) - HC;
+    T v = 0;
+    if (m >= 0 && m < M) {
+      const size_t e = row * M + m;
+      v = g[e];
+      if (h) v -= h[e];
+      if (w) v *= w[(row % n_angles) * M + m];
+    }
+    gt[i] = v;
+  }
+}
+
+template <typename T>
+cudaError_t pad_rows(int n_angles, int M, int B, const T *g, const T *h, const T *w, T *gt, cudaStream_t s) {
+  const size_t total = (size_t)B * n_angles * (M + 2 * HC);
+  const int blocks = (int)std::min<size_t>((total + 255) / 256, 148 * 16);
+  pad_rows_kernel<T><<<blocks, 256, 0, s>>>(n_angles, M, B, g, h, w, gt);
+  return cudaGetLastError();
+}
+template cudaError_t pad_rows<float>(int, int, int, const float *, const float *, const float *, float *, cudaStream_t);
+template cudaError_t pad_rows<double>(int, int, int, const double *, const double *, const double *, double *,
+                                      cudaStream_t);
 
 constexpr int BPT = 64;          // tile edge (pixels)
 constexpr int BP_ROWS = 16;      // rows per thread
@@ -748,9 +785,9 @@ int bp_v2_max_cells(double lx, double ly, double zeta) {
 }
 
 template cudaError_t build_bp_tables<float>(int, int, double, double, double, int, const PPTables<float> &, BPAngle *,
-                                            float *, cudaStream_t);
+                                            float *, cudaStream_t, int);
 template cudaError_t build_bp_tables<double>(int, int, double, double, double, int, const PPTables<double> &,
-                                             BPAngle *, double *, cudaStream_t);
+                                             BPAngle *, double *, cudaStream_t, int);
 template cudaError_t backproject_v2<float>(int, int, int, int, const BPAngle *, const float *, const float *, float *,
                                            int, int, double, cudaStream_t);
 template cudaError_t backproject_v2<double>(int, int, int, int, const BPAngle *, const double *, const double *,

@@ -91,7 +91,15 @@ int bp_v2_max_cells(double lx, double ly, double zeta);  // 0: geometry not supp
 int bp_v2_max_p(int n, const double *angles, double lx, double ly, double zeta);  // host, sub-intervals per cell
 template <typename T>
 cudaError_t build_bp_tables(int N, int M, double lx, double ly, double zeta, int n, const PPTables<T> &tb,
-                            BPAngle *ang, T *Btab, cudaStream_t s);
+                            BPAngle *ang, T *Btab, cudaStream_t s, int interp = 1);
+// gt = pad(w * (g - h)) in K4's [B][n_angles][M + 2 HC] layout (w, h nullable)
+template <typename T>
+cudaError_t pad_rows(int n_angles, int M, int B, const T *g, const T *h, const T *w, T *gt, cudaStream_t s);
+// SIRT helpers (solver.cu): x += C * d (elementwise, C [N*N] broadcast over slices); v -> v > 0 ? 1/v : 0
+template <typename T>
+cudaError_t sirt_update(long n, int B, const T *C, const T *d, T *x, cudaStream_t s);
+template <typename T>
+cudaError_t safe_reciprocal(long n, T *v, cudaStream_t s);
 template <typename T>
 cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
                            int max_cells, int maxP, double scale, cudaStream_t s);

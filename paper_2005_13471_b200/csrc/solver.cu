@@ -172,12 +172,44 @@ cudaError_t spectrum_max(int L, const T *S, double *out, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// SIRT update x[b] += C * d[b] (C: per-pixel weights shared by the slices)
+template <typename T>
+__global__ void __launch_bounds__(256) sirt_update_kernel(long n, int B, const T *__restrict__ C,
+                                                          const T *__restrict__ d, T *__restrict__ x) {
+  const size_t total = (size_t)n * B;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x)
+    x[i] = fma(C[i % n], d[i], x[i]);
+}
+
+template <typename T>
+cudaError_t sirt_update(long n, int B, const T *C, const T *d, T *x, cudaStream_t s) {
+  const size_t total = (size_t)n * B;
+  const int blocks = (int)((total + 255) / 256 < 148 * 16 ? (total + 255) / 256 : 148 * 16);
+  sirt_update_kernel<T><<<blocks, 256, 0, s>>>(n, B, C, d, x);
+  return cudaGetLastError();
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) safe_reciprocal_kernel(long n, T *__restrict__ v) {
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    v[i] = v[i] > (T)0 ? (T)1 / v[i] : (T)0;
+}
+
+template <typename T>
+cudaError_t safe_reciprocal(long n, T *v, cudaStream_t s) {
+  const int blocks = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);
+  safe_reciprocal_kernel<T><<<blocks, 256, 0, s>>>(n, v);
+  return cudaGetLastError();
+}
+
 #define BSCT_SOLVER_INST(T)                                                                                        \
   template cudaError_t solver_init<T>(int, int, const T *, T *, T *, T *, SolverWork, int, cudaStream_t);          \
   template cudaError_t solver_update<T>(int, int, int, int, int, T *, T *, T *, const T *, SolverWork,             \
                                         cudaStream_t);                                                             \
   template cudaError_t solver_finish<T>(int, int, int, int, int, const T *, T *, SolverWork, cudaStream_t);        \
-  template cudaError_t spectrum_max<T>(int, const T *, double *, cudaStream_t);
+  template cudaError_t spectrum_max<T>(int, const T *, double *, cudaStream_t);                                 \
+  template cudaError_t sirt_update<T>(long, int, const T *, const T *, T *, cudaStream_t);                       \
+  template cudaError_t safe_reciprocal<T>(long, T *, cudaStream_t);
 BSCT_SOLVER_INST(float)
 BSCT_SOLVER_INST(double)
 

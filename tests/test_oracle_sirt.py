@@ -36,6 +36,9 @@ def test_adjoint_dot_product():
         lhs = float(np.vdot(forward(g, c), s))
         rhs = float(np.vdot(c, adjoint(g, s)))
         assert abs(lhs - rhs) <= 1e-12 * max(1.0, abs(lhs))
+        k1, k2 = np.array([0, 3, 6, 2]), np.array([6, 3, 0, 5])
+        full = adjoint(g, s)
+        assert np.allclose(adjoint(g, s, pixels=(k1, k2)), full[k1, k2], rtol=1e-13, atol=1e-14)
 
 
 def test_sirt_equals_dense_recurrence_and_monotone():
