@@ -289,7 +289,8 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc(&p->q, sizeof(T) * nn * Bz));
   CU(cudaMalloc((void **)&p->alpha, sizeof(double) * Bz));
   CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * pass_b_blocks(L, p->dt == BSCT_F32)));
-  const size_t nrp = std::max((size_t)vec_blocks(N), (size_t)2 * fused_parts(N, L));
+  // <r,r> partials: room for either pass layout (the warp passes use more CTAs per slice)
+  const size_t nrp = std::max((size_t)vec_blocks(N), (size_t)2 * (fused_parts(N, L, false) + fused_parts(N, L, true)));
   CU(cudaMalloc((void **)&p->rpart, sizeof(double) * Bz * nrp));
   const char *sv1 = getenv("BSCT_SOLVER_V1");
   p->solver_v1 = sv1 && sv1[0] == '1';
@@ -382,7 +383,7 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     // fused iteration (cg.cu): 3 launches per iteration.  Slices are solved in chunks whose
     // per-iteration working set (x, r, p, T1) stays resident in L2, so that the FFT
     // intermediates and the CG vectors cycle through L2 instead of HBM.
-    const int nparts = fused_parts(p->N, p->L);
+    const int nparts = fused_parts(p->N, p->L, p->dt == BSCT_F32);
     const int cb = solver_chunk(p, B);
     auto *T1 = (cplx<T> *)p->T1;
     auto *tw = (const cplx<T> *)p->tw;

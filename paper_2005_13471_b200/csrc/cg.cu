@@ -179,16 +179,16 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N,
 // Z into the two rows' half spectra with lane shuffles (Z[L - q] sits in lane (32 - j) mod
 // 32, register 31 - k), and the CTA writes T1[q][row0 .. row0 + 16) through a [q][9]
 // float4 staging tile (128 contiguous bytes per q).
-template <int VW, bool PLAIN>
-__global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, float *__restrict__ x,
+template <int VW, bool PLAIN, int ROWS>
+__global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(int N, int k, float *__restrict__ x,
                                                                 const float *__restrict__ r,
                                                                 float *__restrict__ p, float2 *__restrict__ T1,
                                                                 const float2 *__restrict__ tw1024, FusedWork w) {
-  constexpr int L = 1024, Q = L / 2 + 1, RS = 9, PW = 512;
+  constexpr int L = 1024, Q = L / 2 + 1, NW = ROWS / 2, RS = NW + 1, PW = 512, NT = 32 * NW;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float *ps = reinterpret_cast<float *>(smem_raw);    // [16][PW] new p rows
+  float *ps = reinterpret_cast<float *>(smem_raw);    // [ROWS][PW] new p rows
   float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] output staging (after the FFTs)
-  float2 *trb = reinterpret_cast<float2 *>(smem_raw); // [8][32][33] transposes
+  float2 *trb = reinterpret_cast<float2 *>(smem_raw); // [NW][32][33] transposes
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.y;
@@ -205,18 +205,18 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, fl
     if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
   }
   const float be = (float)beta, al = (float)alpha_prev;
-  const int row0 = blockIdx.x * 16;
-  const int rows = min(16, N - row0);
+  const int row0 = blockIdx.x * ROWS;
+  const int rows = min(ROWS, N - row0);
   const size_t so = (size_t)b * N * N + (size_t)row0 * N;
   // streaming phase (VW-wide): x += a p_old, p = r + b p_old; p rows -> ps, zero-padded to PW
   // batches of UB items per thread: all 3 UB loads are issued before the first use
-  constexpr int ITEMS = 16 * (PW / VW), UB = 4;
-  for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * 256) {
+  constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
+  for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
     float pv[UB][VW], rv[UB][VW], xv[UB][VW];
     bool ok[UB];
 #pragma unroll
     for (int u = 0; u < UB; ++u) {
-      const int i = i0 + u * 256;
+      const int i = i0 + u * NT;
       const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
       ok[u] = i < ITEMS && rr < rows && j < N;
       if (ok[u]) {
@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, fl
     }
 #pragma unroll
     for (int u = 0; u < UB; ++u) {
-      const int i = i0 + u * 256;
+      const int i = i0 + u * NT;
       if (i >= ITEMS) break;
       const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
       if (ok[u]) {
@@ -278,8 +278,8 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_1024_kernel(int N, int k, fl
   }
   __syncthreads();
   float2 *T1s = T1 + (size_t)b * Q * N + row0;
-  for (int i = threadIdx.x; i < Q * 8; i += blockDim.x) {
-    const int q = i >> 3, pr = i & 7, rp = 2 * pr;
+  for (int i = threadIdx.x; i < Q * NW; i += blockDim.x) {
+    const int q = i / NW, pr = i % NW, rp = 2 * pr;
     if (rp >= rows) continue;
     const float4 e = st[q * RS + pr];
     float2 *dst = T1s + (size_t)q * N + rp;
@@ -398,23 +398,23 @@ __device__ __forceinline__ void cp_async8_g(void *dst, const void *src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(src));
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256, 2) cg_pass_c_1024_kernel(int N, int k, int gparts,
+template <int MODE, int ROWS>
+__global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_c_1024_kernel(int N, int k, int gparts,
                                                                 const float2 *__restrict__ T1,
                                                                 float *__restrict__ x, float *__restrict__ r,
                                                                 const float2 *__restrict__ tw1024, FusedWork w) {
-  constexpr int L = 1024, Q = L / 2 + 1, RS = 9;
+  constexpr int L = 1024, Q = L / 2 + 1, NW = ROWS / 2, RS = NW + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] row pairs, later [8][32][33] float2
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] row pairs, later [NW][32][33] float2
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.y;
-  const int row0 = blockIdx.x * 16;
-  const int rows = min(16, N - row0);
-  // stage T1[q][row0 .. row0 + 16) asynchronously; rows beyond N are zero
+  const int row0 = blockIdx.x * ROWS;
+  const int rows = min(ROWS, N - row0);
+  // stage T1[q][row0 .. row0 + ROWS) asynchronously; rows beyond N are zero
   const float2 *T1s = T1 + (size_t)b * Q * N + row0;
-  for (int i = threadIdx.x; i < Q * 8; i += blockDim.x) {
-    const int q = i >> 3, pr = i & 7, rp = 2 * pr;
+  for (int i = threadIdx.x; i < Q * NW; i += blockDim.x) {
+    const int q = i / NW, pr = i % NW, rp = 2 * pr;
     float4 *dst = st + q * RS + pr;
     const float2 *src = T1s + (size_t)q * N + rp;
     if (rp + 1 < rows) {
@@ -546,7 +546,15 @@ static int fused_parts_L(int N) {
   return (N + 2 * G - 1) / (2 * G);
 }
 
-int fused_parts(int N, int L) {
+// rows per CTA of the FP32 L = 1024 warp-FFT passes A and C (2 rows per warp); 8 rows (4
+// CTAs/SM instead of 2) measured 3% slower on config 5
+#ifndef BSCT_WROWS
+#define BSCT_WROWS 16
+#endif
+constexpr int WROWS = BSCT_WROWS;
+
+int fused_parts(int N, int L, bool fp32) {
+  if (fp32 && L == 1024 && pass_c_warp_enabled()) return (N + WROWS - 1) / WROWS;
   switch (L) {
     case 2: return fused_parts_L<2>(N);
     case 4: return fused_parts_L<4>(N);
@@ -602,15 +610,15 @@ static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx
     if (pass_c_warp_enabled()) {
       const float2 *twl = tw1024_table();
       if (!twl) return cudaErrorMemoryAllocation;
-      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 9;
+      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * (WROWS / 2 + 1);
       if (can_vec<T>(N, x, r, p)) {
-        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, false>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, false, WROWS>, sm);
         if (e != cudaSuccess) return e;
-        cg_pass_a_1024_kernel<4, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_1024_kernel<4, false, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, x, r, p, T1, twl, w);
       } else {
-        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, false>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, false, WROWS>, sm);
         if (e != cudaSuccess) return e;
-        cg_pass_a_1024_kernel<1, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_1024_kernel<1, false, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, x, r, p, T1, twl, w);
       }
       return cudaGetLastError();
     }
@@ -636,10 +644,10 @@ static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *
     if (pass_c_warp_enabled()) {
       const float2 *twl = tw1024_table();
       if (!twl) return cudaErrorMemoryAllocation;
-      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 9;
-      cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<MODE>, sm);
+      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * (WROWS / 2 + 1);
+      cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<MODE, WROWS>, sm);
       if (e != cudaSuccess) return e;
-      cg_pass_c_1024_kernel<MODE><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, gparts, T1, x, r, twl, w);
+      cg_pass_c_1024_kernel<MODE, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, gparts, T1, x, r, twl, w);
       return cudaGetLastError();
     }
   }
@@ -703,19 +711,19 @@ cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaSt
   if (L != 1024 || !pass_c_warp_enabled()) return cudaErrorNotSupported;
   const float2 *twl = tw1024_table();
   if (!twl) return cudaErrorMemoryAllocation;
-  constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * 9;
+  constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * (WROWS / 2 + 1);
   FusedWork w{};
-  w.nparts = fused_parts(N, L);
+  w.nparts = fused_parts(N, L, true);
   w.B = B;
   float *xp = const_cast<float *>(x);
   if (can_vec<float>(N, x, nullptr, nullptr)) {
-    cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, true>, sm);
+    cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, true, WROWS>, sm);
     if (e != cudaSuccess) return e;
-    cg_pass_a_1024_kernel<4, true><<<dim3(w.nparts, B), 256, sm, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
+    cg_pass_a_1024_kernel<4, true, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
   } else {
-    cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, true>, sm);
+    cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, true, WROWS>, sm);
     if (e != cudaSuccess) return e;
-    cg_pass_a_1024_kernel<1, true><<<dim3(w.nparts, B), 256, sm, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
+    cg_pass_a_1024_kernel<1, true, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
   }
   return cudaGetLastError();
 }
@@ -723,13 +731,13 @@ cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaSt
   if (L != 1024 || !pass_c_warp_enabled()) return cudaErrorNotSupported;
   const float2 *twl = tw1024_table();
   if (!twl) return cudaErrorMemoryAllocation;
-  constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * 9;
+  constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * (WROWS / 2 + 1);
   FusedWork w{};
-  w.nparts = fused_parts(N, L);
+  w.nparts = fused_parts(N, L, true);
   w.B = B;
-  cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<3>, sm);
+  cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<3, WROWS>, sm);
   if (e != cudaSuccess) return e;
-  cg_pass_c_1024_kernel<3><<<dim3(w.nparts, B), 256, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w);
+  cg_pass_c_1024_kernel<3, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w);
   return cudaGetLastError();
 }
 

@@ -142,7 +142,7 @@ struct FusedWork {
   int iters;
   double *tau;     // Landweber step (device)
 };
-int fused_parts(int N, int L);
+int fused_parts(int N, int L, bool fp32);  // pass A / C CTAs per slice
 // y = G x with the FP32 L = 1024 warp-FFT passes A and C (cudaErrorNotSupported otherwise)
 cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaStream_t s);
 cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaStream_t s);
