@@ -93,3 +93,29 @@ def landweber(taps, b, iters: int, tau: float | None = None, direct: bool = Fals
 def objective(taps, b, x) -> float:
     """f(x) = 1/2 <x, Gx> - <b, x> (monotone in CG/SD; SURVEY.md R12 guard)."""
     return 0.5 * float(np.vdot(x, apply_fft(taps, x))) - float(np.vdot(b, x))
+
+
+def chebyshev(taps, b, iters: int, lmin: float, lmax: float, direct: bool = False):
+    """Chebyshev semi-iteration for G x = b with spectrum assumed in [lmin, lmax] (SURVEY.md
+    8(f) NEXT-4; Saad, Iterative Methods for Sparse Linear Systems, 2nd ed., Alg. 12.1):
+        theta = (lmax + lmin)/2, delta = (lmax - lmin)/2, sigma = theta/delta,
+        x0 = 0, r0 = b, rho0 = 1/sigma, d0 = r0/theta;
+        x_{k+1} = x_k + d_k, r_{k+1} = r_k - G d_k,
+        rho_{k+1} = 1/(2 sigma - rho_k), d_{k+1} = rho_{k+1} rho_k d_k + (2 rho_{k+1}/delta) r_{k+1}.
+    No inner products: x_k is a fixed polynomial in G applied to b (linear in b)."""
+    b = np.asarray(b, dtype=np.float64)
+    theta, delta = 0.5 * (lmax + lmin), 0.5 * (lmax - lmin)
+    sigma = theta / delta
+    x = np.zeros_like(b)
+    r = b.copy()
+    rho = 1.0 / sigma
+    d = r / theta
+    hist = []
+    for _ in range(iters):
+        x = x + d
+        r = r - _apply(taps, d, direct)
+        rho_n = 1.0 / (2.0 * sigma - rho)
+        d = rho_n * rho * d + (2.0 * rho_n / delta) * r
+        rho = rho_n
+        hist.append(np.sqrt(float(np.vdot(r, r))))
+    return x, np.array(hist)

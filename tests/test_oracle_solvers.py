@@ -75,3 +75,49 @@ def test_zero_rhs():
     T, b = problem()
     x, h = solvers.cg(T, np.zeros_like(b), 5)
     assert not x.any() and not h.any()
+
+
+def _dense_G(taps, N):
+    from oracle.normal import apply_direct
+    cols = []
+    for k in range(N * N):
+        e = np.zeros((N, N))
+        e.flat[k] = 1.0
+        cols.append(apply_direct(taps, e).ravel())
+    return np.stack(cols, axis=1)
+
+
+def test_chebyshev_residual_polynomial():
+    """r_k = T_k((theta - G)/delta) b / T_k(theta/delta) (Chebyshev polynomial identity, checked
+    through the eigendecomposition of the dense Toeplitz operator), and the minimax bound
+    ||r_k|| <= ||b|| / T_k(theta/delta) when the spectrum lies in [lmin, lmax]."""
+    from numpy.polynomial import chebyshev as C
+    from oracle.gram import gram_taps
+    from oracle.solvers import chebyshev
+    g = dict(N=6, lambda_x=1.0, angles=np.arange(12) * np.pi / 12, lambda_y=1.0, n_det=13, zeta=1.0)
+    T = gram_taps(g)
+    G = _dense_G(T, 6)
+    lam, V = np.linalg.eigh(G)
+    b = np.random.default_rng(4).standard_normal((6, 6))
+    for lmin, lmax in ((lam[0], lam[-1]), (0.5 * lam[0], 1.2 * lam[-1])):
+        theta, delta = 0.5 * (lmax + lmin), 0.5 * (lmax - lmin)
+        for k in (1, 3, 7):
+            x, hist = chebyshev(T, b, k, lmin, lmax, direct=True)
+            ck = np.zeros(k + 1)
+            ck[k] = 1.0
+            pk = C.chebval((theta - lam) / delta, ck) / C.chebval(theta / delta, ck)
+            r_pred = V @ (pk * (V.T @ b.ravel()))
+            r = b.ravel() - G @ x.ravel()
+            assert np.abs(r - r_pred).max() < 1e-10 * np.abs(b).max()
+            assert hist[-1] <= np.linalg.norm(b) / C.chebval(theta / delta, ck) * (1 + 1e-10)
+
+
+def test_chebyshev_exact_interval_one_point():
+    """lmin = lmax = G00 on N = 1: d0 = b / G00 and x_1 = b / G00 exactly."""
+    from oracle.gram import gram_taps
+    from oracle.solvers import chebyshev
+    g = dict(N=1, lambda_x=1.0, angles=np.arange(4) * np.pi / 4, lambda_y=1.0, n_det=5, zeta=0.0)
+    T = gram_taps(g)
+    lam = float(T[0, 0])
+    x, _ = chebyshev(T, np.array([[3.0]]), 1, lam * (1 - 1e-9), lam * (1 + 1e-9), direct=True)
+    assert x[0, 0] == pytest.approx(3.0 / lam, rel=1e-8)
