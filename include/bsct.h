@@ -156,6 +156,17 @@ bsct_status bsct_cg_solve(bsct_plan plan, const void *b, void *x, int32_t B, int
 bsct_status bsct_forward_project(bsct_plan plan, const void *c, void *sino, int32_t B, bsct_stream stream);
 
 /*
+ * Chebyshev semi-iteration for G x = b (NEXT-4; Saad, Alg. 12.1), spectrum assumed in
+ * [lambda_min, lambda_max]: no inner products, so x_k is a fixed polynomial in G applied to b
+ * (linear in b; FP32 iterates keep parity with FP64).  lambda_max <= 0 takes the plan's bound
+ * max(DFT of the L x L embedding) >= lambda_max(G) (interlacing).  Requires
+ * 0 < lambda_min < lambda_max (BSCT_EINVAL).  Per iteration: the three FFT passes of
+ * bsct_normal_apply + one update kernel.  resid_hist: DEVICE [B][iters] ||r_k|| or NULL.
+ */
+bsct_status bsct_chebyshev_solve(bsct_plan plan, const void *b, void *x, int32_t B, int32_t iters,
+                                 double lambda_min, double lambda_max, double *resid_hist, bsct_stream stream);
+
+/*
  * Plain adjoint of the sampled forward model (SIRT's back projection; NEXT-1):
  *     img[k] = lambda_x^2 sum_t sum_m sino[t][m] M_[l|c|, l|s|, zeta](y_m - k_t)
  * i.e. the transpose of bsct_forward_project (no correction filter, no interpolant --

@@ -35,7 +35,7 @@ H_CORR = 25
 SYMBOLS = ("bsct_version", "bsct_last_error", "bsct_fft_size", "bsct_gram_build", "bsct_plan_create",
            "bsct_plan_destroy", "bsct_plan_set_filter", "bsct_plan_spectrum", "bsct_correction_filter", "bsct_backproject",
            "bsct_normal_apply", "bsct_cg_solve", "bsct_forward_project", "bsct_reconstruct", "bsct_reconstruct_host",
-           "bsct_adjoint_project", "bsct_sirt_solve",
+           "bsct_adjoint_project", "bsct_sirt_solve", "bsct_chebyshev_solve",
            "bsct_plan_launch_count", "bsct_plan_profile", "bsct_plan_profile_read")
 
 # bsct_kernel_class
@@ -86,6 +86,7 @@ def load(path: str | None = None):
         "bsct_reconstruct": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "bsct_adjoint_project": (i32, [vp, vp, vp, i32, vp]),
         "bsct_sirt_solve": (i32, [vp, vp, vp, i32, i32, vp]),
+        "bsct_chebyshev_solve": (i32, [vp, vp, vp, i32, i32, dp, dp, vp, vp]),
         "bsct_reconstruct_host": (i32, [vp, vp, vp, i32, i32, i32, vp]),
         "bsct_plan_launch_count": (i64, [vp]),
         "bsct_plan_profile": (i32, [vp, i32]),
@@ -279,6 +280,19 @@ def reconstruct(plan: Plan, sino, x, iters: int, solver="cg", resid_hist=None, f
                                    _ptr(x, plan.dtype, B * plan.N * plan.N, "x"), B, int(iters), sv,
                                    _ptr(resid_hist, torch.float64, B * iters, "resid_hist"),
                                    _ptr(flags, torch.int32, B, "flags"), _stream(stream)))
+    return x
+
+
+def chebyshev_solve(plan: Plan, b, x, iters: int, lambda_min: float, lambda_max: float = 0.0,
+                    resid_hist=None, stream=None):
+    """x[B,N,N] <- `iters` Chebyshev semi-iterations on G x = b (spectrum in [lambda_min,
+    lambda_max]; lambda_max <= 0: the plan's embedding-spectrum bound)."""
+    import torch
+    B = _batch(b, plan.N * plan.N, "b")
+    _check(load().bsct_chebyshev_solve(plan.handle, _ptr(b, plan.dtype, name="b"),
+                                       _ptr(x, plan.dtype, B * plan.N * plan.N, "x"), B, int(iters),
+                                       float(lambda_min), float(lambda_max),
+                                       _ptr(resid_hist, torch.float64, B * iters, "resid_hist"), _stream(stream)))
     return x
 
 

@@ -523,11 +523,53 @@ bsct_status sirt_t(bsct_plan p, const T *sino, T *x, int B, int iters, cudaStrea
   return BSCT_OK;
 }
 
+// Chebyshev semi-iteration (oracle/solvers.py chebyshev): per iteration y = G d (the same three
+// FFT passes as bsct_normal_apply) and one update kernel; coefficients from the host.
+template <typename T>
+bsct_status chebyshev_t(bsct_plan p, const T *b, T *x, int B, int iters, double lmin, double lmax, double *resid,
+                        cudaStream_t s) {
+  const double theta = 0.5 * (lmax + lmin), delta = 0.5 * (lmax - lmin), sigma = theta / delta;
+  T *r = (T *)p->r, *d = (T *)p->p, *y = (T *)p->q;
+  LAUNCH(p, BSCT_K_SOLVER_INIT, 1, (cheb_init<T>(p->N, B, b, x, r, d, 1.0 / theta, s)));
+  double rho = 1.0 / sigma;
+  for (int it = 0; it < iters; ++it) {
+    bsct_status st = normal_apply_t<T>(p, d, y, B, nullptr, s);
+    if (st != BSCT_OK) return st;
+    const double rn = 1.0 / (2.0 * sigma - rho);
+    LAUNCH(p, BSCT_K_SOLVER_UPDATE, resid ? 2 : 1,
+           (cheb_update<T>(p->N, B, rn * rho, 2.0 * rn / delta, x, r, d, y, p->rpart, resid, iters, it, s)));
+    rho = rn;
+  }
+  return BSCT_OK;
+}
+
 }  // namespace
 
 extern "C" {
 
 int32_t bsct_version(void) { return 100; }
+
+bsct_status bsct_chebyshev_solve(bsct_plan p, const void *b, void *x, int32_t B, int32_t iters, double lambda_min,
+                                 double lambda_max, double *resid_hist, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (!(lambda_max > 0)) {  // the plan's bound: max of the embedding spectrum >= lambda_max(G)
+    double tau = 0;
+    CU(cudaMemcpyAsync(&tau, p->tau, sizeof(double), cudaMemcpyDeviceToHost, s));
+    CU(cudaStreamSynchronize(s));
+    lambda_max = 1.0 / tau;
+  }
+  if (!(lambda_min > 0) || !(lambda_min < lambda_max) || !std::isfinite(lambda_max))
+    return fail(BSCT_EINVAL, "need 0 < lambda_min < lambda_max (got %g, %g)", lambda_min, lambda_max);
+  if (B == 0) return BSCT_OK;
+  if (!b || !x) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  return p->dt == BSCT_F64
+             ? chebyshev_t<double>(p, (const double *)b, (double *)x, B, iters, lambda_min, lambda_max, resid_hist, s)
+             : chebyshev_t<float>(p, (const float *)b, (float *)x, B, iters, lambda_min, lambda_max, resid_hist, s);
+}
 
 bsct_status bsct_adjoint_project(bsct_plan p, const void *sino, void *img, int32_t B, bsct_stream stream) {
   bsct_status st = check_plan(p, B);

@@ -100,6 +100,12 @@ template <typename T>
 cudaError_t sirt_update(long n, int B, const T *C, const T *d, T *x, cudaStream_t s);
 template <typename T>
 cudaError_t safe_reciprocal(long n, T *v, cudaStream_t s);
+// Chebyshev semi-iteration (solver.cu): x = 0, r = b, d = b / theta; x += d, r -= y, d = c1 d + c2 r
+template <typename T>
+cudaError_t cheb_init(int N, int B, const T *b, T *x, T *r, T *d, double inv_theta, cudaStream_t s);
+template <typename T>
+cudaError_t cheb_update(int N, int B, double c1, double c2, T *x, T *r, T *d, const T *y, double *rpart,
+                        double *resid, int iters, int k, cudaStream_t s);
 template <typename T>
 cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang, const T *Btab, const T *gt, T *b,
                            int max_cells, int maxP, double scale, cudaStream_t s);

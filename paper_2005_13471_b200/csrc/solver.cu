@@ -202,6 +202,66 @@ cudaError_t safe_reciprocal(long n, T *v, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// ---- Chebyshev semi-iteration (NEXT-4, oracle/solvers.py chebyshev): coefficients are a fixed
+// host-computed sequence; per iteration y = G d (normal apply), then this update.
+// init: x = 0, r = b, d = b / theta
+template <typename T>
+__global__ void __launch_bounds__(VT) cheb_init_kernel(long n, const T *__restrict__ b, T *__restrict__ x,
+                                                       T *__restrict__ r, T *__restrict__ d, double inv_theta) {
+  const size_t off = (size_t)blockIdx.y * n;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const T v = b[off + i];
+    x[off + i] = 0;
+    r[off + i] = v;
+    d[off + i] = (T)((double)v * inv_theta);
+  }
+}
+
+// x += d; r -= y; d = c1 d + c2 r; partials of <r, r> per (slice, CTA) when rpart != null
+template <typename T>
+__global__ void __launch_bounds__(VT) cheb_update_kernel(long n, T c1, T c2, T *__restrict__ x, T *__restrict__ r,
+                                                         T *__restrict__ d, const T *__restrict__ y,
+                                                         double *__restrict__ rpart) {
+  __shared__ double red[32];
+  const size_t off = (size_t)blockIdx.y * n;
+  double acc = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const size_t e = off + i;
+    const T dv = d[e];
+    x[e] += dv;
+    const T rv = r[e] - y[e];
+    r[e] = rv;
+    d[e] = fma(c1, dv, c2 * rv);
+    acc += (double)rv * rv;
+  }
+  if (rpart) {
+    const double sm = block_sum(acc, red);
+    if (threadIdx.x == 0) rpart[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = sm;
+  }
+}
+
+__global__ void __launch_bounds__(VT) cheb_resid_kernel(const double *__restrict__ rpart, int nparts, double *resid,
+                                                        int iters, int k) {
+  __shared__ double red[32];
+  const double s = reduce_parts(rpart + (size_t)blockIdx.x * nparts, nparts, red);
+  if (threadIdx.x == 0) resid[(size_t)blockIdx.x * iters + k] = sqrt(s);
+}
+
+template <typename T>
+cudaError_t cheb_init(int N, int B, const T *b, T *x, T *r, T *d, double inv_theta, cudaStream_t s) {
+  cheb_init_kernel<T><<<dim3(vec_blocks(N), B), VT, 0, s>>>((long)N * N, b, x, r, d, inv_theta);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t cheb_update(int N, int B, double c1, double c2, T *x, T *r, T *d, const T *y, double *rpart,
+                        double *resid, int iters, int k, cudaStream_t s) {
+  const int vb = vec_blocks(N);
+  cheb_update_kernel<T><<<dim3(vb, B), VT, 0, s>>>((long)N * N, (T)c1, (T)c2, x, r, d, y, resid ? rpart : nullptr);
+  if (resid) cheb_resid_kernel<<<B, VT, 0, s>>>(rpart, vb, resid, iters, k);
+  return cudaGetLastError();
+}
+
 #define BSCT_SOLVER_INST(T)                                                                                        \
   template cudaError_t solver_init<T>(int, int, const T *, T *, T *, T *, SolverWork, int, cudaStream_t);          \
   template cudaError_t solver_update<T>(int, int, int, int, int, T *, T *, T *, const T *, SolverWork,             \
@@ -209,7 +269,10 @@ cudaError_t safe_reciprocal(long n, T *v, cudaStream_t s) {
   template cudaError_t solver_finish<T>(int, int, int, int, int, const T *, T *, SolverWork, cudaStream_t);        \
   template cudaError_t spectrum_max<T>(int, const T *, double *, cudaStream_t);                                 \
   template cudaError_t sirt_update<T>(long, int, const T *, const T *, T *, cudaStream_t);                       \
-  template cudaError_t safe_reciprocal<T>(long, T *, cudaStream_t);
+  template cudaError_t safe_reciprocal<T>(long, T *, cudaStream_t);                                             \
+  template cudaError_t cheb_init<T>(int, int, const T *, T *, T *, T *, double, cudaStream_t);                  \
+  template cudaError_t cheb_update<T>(int, int, double, double, T *, T *, T *, const T *, double *, double *,    \
+                                      int, int, cudaStream_t);
 BSCT_SOLVER_INST(float)
 BSCT_SOLVER_INST(double)
 

@@ -174,3 +174,32 @@ def test_reconstruct_pipeline_equals_sequence(cuda_lib, chunk, overlap, solver, 
     xh = torch.empty((B, 64, 64), dtype=torch.float32).pin_memory()
     cuda_lib.reconstruct_host(plan, torch.from_numpy(sino).pin_memory(), xh, 7, solver)
     assert torch.equal(xh, x.cpu())
+
+
+@pytest.mark.parametrize("ci,iters,tl", [(1, 20, 1e-9), (2, 50, 1e-4), (3, 100, 1e-3)])  # 1e-3: north_star reconstructions
+def test_chebyshev(cuda_lib, ci, iters, tl):
+    """NEXT-4: Chebyshev semi-iteration vs the FP64 oracle at the config's iteration count.  No
+    inner products, so unlike FP32 CG (R12) the FP32 iterates keep parity with FP64; the
+    interval is [lambda_max / 1e3, lambda_max], lambda_max = max of the embedding spectrum."""
+    import torch
+    cfg = CONFIGS[ci]
+    T = gram_taps(cfg.geometry())
+    b = rhs(cfg, T)
+    lmax = 1.0 / solvers.landweber_tau(T)
+    lmin = lmax / 1e3
+    g = cfg.geometry()
+    plan, taps = gpu_plan(cuda_lib, g, cfg.dtype, max_batch=1)
+    x = torch.empty((1, cfg.N, cfg.N), dtype=taps.dtype, device="cuda")
+    h = torch.empty((1, iters), dtype=torch.float64, device="cuda")
+    cuda_lib.chebyshev_solve(plan, to_dev(b, cfg.dtype), x, iters, lmin, lmax, resid_hist=h)
+    torch.cuda.synchronize()
+    xr, hr = solvers.chebyshev(T, b[0], iters, lmin, lmax)
+    assert rel_l2(to_np(x[0]), xr) < tl
+    assert rel_l2(h.cpu().numpy()[0], hr) < tl
+    # the plan's own spectrum bound (lambda_max <= 0) gives the same iterate up to FP rounding
+    x2 = torch.empty_like(x)
+    cuda_lib.chebyshev_solve(plan, to_dev(b, cfg.dtype), x2, iters, lmin)
+    torch.cuda.synchronize()
+    assert rel_l2(to_np(x2[0]), xr) < 10 * tl
+    with pytest.raises(cuda_lib.BsctError):
+        cuda_lib.chebyshev_solve(plan, to_dev(b, cfg.dtype), x2, iters, lmax * 2, lmax)
