@@ -128,6 +128,9 @@ __global__ void __launch_bounds__(FftLaunchB<L>::THREADS) pass_b_kernel(int N, c
 // formed.  No block-wide barrier; PB_WARPS columns per CTA share the W_1024 table.
 constexpr int PB_WARPS = 4;
 
+// FULL: N == L / 2 (every load and store in range, no per-element guards; halves the code the
+// compiler emits, which otherwise versions the FFT body on the guards)
+template <bool FULL>
 __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, float2 *__restrict__ T1,
                                                                   const float *__restrict__ S,
                                                                   const float2 *__restrict__ tw1024,
@@ -140,15 +143,20 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
   for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) twl[i] = tw1024[i];
   __syncthreads();
   const int b = blockIdx.y;
-  const int q = blockIdx.x * PB_WARPS + warp;
+  // warps past the last column recompute column Q - 1 and store nothing: no branch around the
+  // FFT (its __syncwarp transposes in possibly-divergent code made the compiler emit a second,
+  // divergent-path copy of the whole body)
+  const int q0 = blockIdx.x * PB_WARPS + warp;
+  const bool live = q0 < Q;
+  const int q = live ? q0 : Q - 1;
   double gam = 0.0;
-  if (q < Q) {
+  {
     float2 *col = T1 + ((size_t)b * Q + q) * N;
     float2 v[32];
 #pragma unroll
     for (int r = 0; r < 16; ++r) {
       const int n = lane + 32 * r;
-      v[r] = n < N ? col[n] : float2{0.f, 0.f};
+      v[r] = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
     }
     dft32<false, true>(v);  // over r (v[16..31] = 0): v[j] = sum_r x[lane + 32 r] W_32^{r j}
 #pragma unroll
@@ -168,6 +176,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
     }
     gam = (double)(g4[0] + g4[1]) + (double)(g4[2] + g4[3]);
     if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
+    if (!live) gam = 0.0;
     dft32<true>(v);  // over k: v[a] = U[lane][a]
 #pragma unroll
     for (int a = 1; a < 32; ++a) v[a] = cmulc(v[a], twl[a * 32 + lane]);
@@ -176,7 +185,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
       const int n = lane + 32 * m;
-      if (n < N) col[n] = v[m];
+      if (live && (FULL || n < N)) col[n] = v[m];
     }
   }
   if (gpart) {  // deterministic CTA reduction
@@ -378,8 +387,11 @@ static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T>
     const float2 *twl = tw1024_table();
     if (!twl) return cudaErrorMemoryAllocation;
     if (pass_b_warp_enabled()) {
-      pass_b_1024_kernel<<<dim3((L / 2 + 1 + PB_WARPS - 1) / PB_WARPS, B), PB_WARPS * 32, 0, s>>>(
-          N, T1, S, twl, gpart);
+      const dim3 grid((L / 2 + 1 + PB_WARPS - 1) / PB_WARPS, B);
+      if (N == L / 2)
+        pass_b_1024_kernel<true><<<grid, PB_WARPS * 32, 0, s>>>(N, T1, S, twl, gpart);
+      else
+        pass_b_1024_kernel<false><<<grid, PB_WARPS * 32, 0, s>>>(N, T1, S, twl, gpart);
       return cudaGetLastError();
     }
   }
