@@ -271,6 +271,13 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc((void **)&p->tau, sizeof(double)));
   const char *force_v1 = getenv("BSCT_BP_V1");
   p->bp_cells = (force_v1 && force_v1[0] == '1') ? 0 : bp_v2_max_cells(p->lx, p->ly, p->zeta);
+  if (p->bp_cells > 0) {
+    // K4 v2's double-buffered tables must fit in shared memory (fine detectors, lambda_y << lambda_x,
+    // have many cells per tile); otherwise K4 v1 (direct per-sample evaluation)
+    const size_t buf = (size_t)p->bp_cells * (p->bp_maxp * 8 + 4) + p->bp_maxp * BP_SMAX * 8 +
+                       ((p->bp_cells + BP_SMAX + 7) & ~7);
+    if (p->esize() * 2 * buf > 227 * 1024) p->bp_cells = 0;
+  }
   const char *bp2 = getenv("BSCT_BP_V2");
   p->bp_v3 = !(bp2 && bp2[0] == '1');
   if (p->bp_cells > 0) {

@@ -41,7 +41,8 @@ def test_correction_filter(cuda_lib, zeta, ly, dt):
 
 @pytest.mark.parametrize("N,n,M,ly,zeta,dt,B", [
     (1, 3, 5, 1.0, 0.0, "f32", 1), (4, 8, 9, 1.0, 1.0, "f64", 2), (7, 11, 15, 0.5, 0.5, "f32", 2),
-    (16, 24, 33, 1.0, 0.0, "f32", 1), (16, 24, 23, 1.3, 1.7, "f64", 1), (33, 36, 49, 1.0, 1.5, "f32", 2)])
+    (16, 24, 33, 1.0, 0.0, "f32", 1), (16, 24, 23, 1.3, 1.7, "f64", 1), (33, 36, 49, 1.0, 1.5, "f32", 2),
+    (20, 12, 121, 0.25, 0.25, "f32", 2)])  # fine detector: K4 v2 tables exceed smem -> K4 v1
 def test_small_full(cuda_lib, N, n, M, ly, zeta, dt, B):
     g = geom(N, uniform(n), M, lambda_y=ly, zeta=zeta)
     sino = random_sinogram(N + n, B, n, M)
