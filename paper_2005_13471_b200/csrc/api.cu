@@ -443,7 +443,10 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
 template <typename T>
 bsct_status forward_t(bsct_plan p, const T *c, T *sino, int B, cudaStream_t s) {
   PPTables<T> fw = tables_of<T>(p->fw_mem, p->n_angles);
-  LAUNCH(p, BSCT_K_FORWARD, 1, (forward_project<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, fw.cs, fw.view(), c, sino, s)));
+  // the plan's q workspace holds the transposed image (it is free outside a solve; SIRT overwrites
+  // it only after the forward projection)
+  LAUNCH(p, BSCT_K_FORWARD, 2,
+         (forward_project<T>(p->N, p->lx, p->ly, p->n_angles, p->M, B, fw.cs, fw.view(), c, sino, s, (T *)p->q)));
   return BSCT_OK;
 }
 

@@ -61,29 +61,46 @@ __global__ void __launch_bounds__(256) forward_kernel(int N, double lx, double l
   sino[((size_t)b * n_angles + a) * M + m] = (T)(lx * lx) * acc;
 }
 
-// K7 v2.  Same sums as forward_kernel, same order (ascending line, then ascending pixel
-// within the strip), but: one CTA per (angle, slice) with the angle's right-half table
-// (<= FWD_MAXP pieces of degree <= 2: the box spline of <= 3 widths) in shared memory;
-// FP64 only once per line of pixels (the strip bounds and the argument at its first
-// pixel); along the strip the argument steps by the per-pixel advance in T (<= ~8 steps
-// from an FP64 anchor, so the argument error stays ~1e-6 of a detector cell); piece
-// selection by register compares; no binary search in global memory.
+// K7 v3.  Same sums as forward_kernel, same order (ascending line, then ascending pixel
+// within the strip).  One CTA per (angle, slice) with the angle's right-half table (<= FWD_MAXP
+// pieces of degree <= 2: the box spline of <= 3 widths) in shared memory.  Lines are image rows
+// when |cos t| >= |sin t| and rows of the transposed image otherwise, so the lanes of a warp
+// (consecutive detector samples) always read neighbouring pixels of one row.  Per line the strip
+// bounds advance by a constant in FP64 and are rounded with the 1.5 * 2^52 trick (no conversion
+// instructions); the argument at the strip's first pixel, H + st (e - j0) with e - j0 exact, is
+// the one FP64 -> T conversion; along the strip the argument steps by st in T (<= ~8 steps).
 constexpr int FWD_MAXP = 8;
+constexpr double FWD_MAGIC = 6755399441055744.0;  // 1.5 * 2^52
 
 template <typename T>
-__global__ void __launch_bounds__(256) forward_v2_kernel(int N, double lx, double ly, int n_angles, int M,
+__global__ void __launch_bounds__(256) transpose_kernel(int N, const T *__restrict__ c, T *__restrict__ ct) {
+  __shared__ T t[32][33];
+  const int b = blockIdx.z;
+  const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 32;
+  const T *src = c + (size_t)b * N * N;
+  T *dst = ct + (size_t)b * N * N;
+  for (int r = threadIdx.y; r < 32; r += 8)
+    if (y0 + r < N && x0 + threadIdx.x < N) t[r][threadIdx.x] = src[(size_t)(y0 + r) * N + x0 + threadIdx.x];
+  __syncthreads();
+  for (int r = threadIdx.y; r < 32; r += 8)
+    if (x0 + r < N && y0 + threadIdx.x < N) dst[(size_t)(x0 + r) * N + y0 + threadIdx.x] = t[threadIdx.x][r];
+}
+
+template <typename T, int PC>
+__global__ void __launch_bounds__(256) forward_v3_kernel(int N, double lx, double ly, int n_angles, int M,
                                                          const double *__restrict__ cs, PPView<T> tb,
-                                                         const T *__restrict__ c, T *__restrict__ sino) {
+                                                         const T *__restrict__ c, const T *__restrict__ ct,
+                                                         T *__restrict__ sino) {
   const int a = blockIdx.x, b = blockIdx.y;
   __shared__ T kn_s[FWD_MAXP + 1], cf_s[FWD_MAXP][3];
-  __shared__ int np_s, nw_s;
+  __shared__ int nw_s;
   const int np = tb.npieces[a];
   if (threadIdx.x <= FWD_MAXP) kn_s[threadIdx.x] = threadIdx.x <= np ? (T)tb.knots[(size_t)a * (PP_MAXP + 1) + threadIdx.x] : (T)3e38;
   if (threadIdx.x < FWD_MAXP * 3) {
     const int j = threadIdx.x / 3, k = threadIdx.x % 3;
     cf_s[j][k] = j < np ? tb.coef[((size_t)a * PP_MAXP + j) * PP_NC + k] : (T)0;
   }
-  if (threadIdx.x == 0) { np_s = np; nw_s = tb.nwidths[a]; }
+  if (threadIdx.x == 0) nw_s = tb.nwidths[a];
   __syncthreads();
   const double co = cs[2 * a], si = cs[2 * a + 1];
   const double H = tb.half[a];
@@ -102,33 +119,58 @@ __global__ void __launch_bounds__(256) forward_v2_kernel(int N, double lx, doubl
     const T t = ax - kn_s[j];
     return fma(fma(cf_s[j][2], t, cf_s[j][1]), t, cf_s[j][0]);
   };
-  const T *img = c + (size_t)b * N * N;
-  const int h = N / 2;
   const bool rows = fabs(co) >= fabs(si);
-  // lines: rows k1 (pixels k2 along the row) or columns k2 (pixels k1 along the column);
-  // arg(line, j) = A(line) - st * j with A(line) = y - kt(line, 0), st = d kt / d j
+  const T *img = (rows ? c : ct) + (size_t)b * N * N;  // line l = row l of img, pixels j along it
+  const int h = N / 2;
+  // arg(l, j) = A(l) - st j;  A(l) = A0 + l dA  (rows: kt = -si x1 + co x2 with x1 = lx (l - h),
+  // x2 = lx (j - h); columns: x2 = lx (l - h), x1 = lx (j - h))
   const double st = rows ? co * lx : -si * lx;
+  const double dA = rows ? si * lx : -co * lx;
+  const double A0c = rows ? -si * lx * h + co * lx * h : co * lx * h - si * lx * h;  // A0 = y + A0c
   const double inv = 1.0 / st;
+  const double sH = st > 0 ? H : -H;  // e_lo = (A - sH)/st is the lower strip end
   const T stT = (T)st;
+  const T box = (T)(0.5 / H);  // one width: M = 1/w on [-w/2, w/2) (R6)
+  const double de = dA * inv;
+  // pixels per line in the strip: j in (e_lo, e_lo + 2H/|st|) -> at most KS = floor(2H/|st|) + 2
+  // candidates from j0 = floor(e_lo) (uniform across the CTA: no divergent inner loops)
+  const int KS = (int)(2.0 * H / fabs(st)) + 2;
+  // the strip is non-empty in line l iff e_lo(l) < N and e_lo(l) + 2H/|st| > -1: a contiguous
+  // range of l (e_lo is linear in l), computed per sample
+  const double w = 2.0 * H * fabs(inv);
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
     const double y = ly * (double)(m - M / 2);
+    const double e00 = (y + A0c - sH) * inv;  // e_lo at l = 0
+    int l0 = 0, l1 = N - 1;
+    if (de != 0.0) {
+      // e_lo(l) = e00 + l de; need -1 - w < e_lo(l) < N
+      double la = (-1.0 - w - e00) / de, lb = ((double)N - e00) / de;
+      if (la > lb) { const double tt = la; la = lb; lb = tt; }
+      l0 = max(0, (int)floor(la));
+      l1 = min(N - 1, (int)ceil(lb));
+    } else if (!(e00 < N && e00 + w > -1.0)) {
+      l1 = -1;
+    }
     T acc = 0;
-    for (int l = 0; l < N; ++l) {
-      const double xl = lx * (double)(l - h);
-      // kt(l, j) = rows ? (-si xl + co lx (j - h)) : (-si lx (j - h) + co xl)
-      const double A = rows ? y + si * xl + co * lx * h : y - co * xl - si * lx * h;
-      // |A - st j| < H  <=>  j in ((A - H)/st, (A + H)/st) (interval ends swap for st < 0)
-      const double e0 = (A - H) * inv, e1 = (A + H) * inv;
-      int j0 = (int)floor(fmin(e0, e1)), j1 = (int)ceil(fmax(e0, e1));
-      j0 = max(0, j0);
-      j1 = min(N - 1, j1);
-      if (j0 > j1) continue;
-      T arg = (T)(A - st * (double)j0);
-      const T *line = rows ? img + (size_t)l * N : img + l;
-      const size_t step = rows ? 1 : (size_t)N;
-      for (int j = j0; j <= j1; ++j, arg -= stT) {
-        const T v = eval(arg);
-        if (v != (T)0) acc = fma(line[(size_t)j * step], v, acc);
+    double elo = e00 + (double)l0 * de;
+    for (int l = l0; l <= l1; ++l, elo += de) {
+      const double t0 = (elo - 0.5) + FWD_MAGIC;
+      const int j0 = __double2loint(t0);             // ~floor(e_lo)
+      const double f0 = elo - (t0 - FWD_MAGIC);      // e_lo - j0, exact
+      T arg = (T)(sH + st * f0);                      // arg at j = j0
+      const T *line = img + (size_t)l * N;
+      for (int k = 0; k < KS; ++k, arg -= stT) {
+        const int j = j0 + k;
+        // branch-free M(arg): piece by compares, zero outside [-H, H) and outside the image
+        const T ax = fabs(arg);
+        int q = 0;
+#pragma unroll
+        for (int qq = 1; qq <= PC; ++qq) q += (ax >= kn[qq]) ? 1 : 0;
+        const T tq = ax - kn_s[q];
+        const T v = nw == 1 ? box : fma(fma(cf_s[q][2], tq, cf_s[q][1]), tq, cf_s[q][0]);
+        const bool sup = nw == 1 ? (arg >= -Ht && arg < Ht) : (ax < Ht);
+        const bool in = sup && (unsigned)j < (unsigned)N;
+        if (in) acc = fma(line[j], v, acc);
       }
     }
     sino[((size_t)b * n_angles + a) * M + m] = (T)(lx * lx) * acc;
@@ -137,20 +179,23 @@ __global__ void __launch_bounds__(256) forward_v2_kernel(int N, double lx, doubl
 
 template <typename T>
 cudaError_t forward_project(int N, double lx, double ly, int n_angles, int M, int B, const double *cs,
-                            PPView<T> tb, const T *c, T *sino, cudaStream_t s) {
+                            PPView<T> tb, const T *c, T *sino, cudaStream_t s, T *work) {
   const char *v1 = getenv("BSCT_FWD_V1");
   if (v1 && v1[0] == '1') {
     dim3 grid((M + 255) / 256, n_angles, B);
     forward_kernel<T><<<grid, 256, 0, s>>>(N, lx, ly, n_angles, M, cs, tb, c, sino);
   } else {
-    forward_v2_kernel<T><<<dim3(n_angles, B), 256, 0, s>>>(N, lx, ly, n_angles, M, cs, tb, c, sino);
+    if (!work) return cudaErrorInvalidValue;  // [B][N][N] scratch for the transposed image
+    transpose_kernel<T><<<dim3((N + 31) / 32, (N + 31) / 32, B), dim3(32, 8), 0, s>>>(N, c, work);
+    // the forward model's box spline has <= 3 widths: <= 5 right-half pieces, 4 knot compares
+    forward_v3_kernel<T, 4><<<dim3(n_angles, B), 256, 0, s>>>(N, lx, ly, n_angles, M, cs, tb, c, work, sino);
   }
   return cudaGetLastError();
 }
 
 template cudaError_t forward_project<float>(int, double, double, int, int, int, const double *, PPView<float>,
-                                            const float *, float *, cudaStream_t);
+                                            const float *, float *, cudaStream_t, float *);
 template cudaError_t forward_project<double>(int, double, double, int, int, int, const double *, PPView<double>,
-                                             const double *, double *, cudaStream_t);
+                                             const double *, double *, cudaStream_t, double *);
 
 }  // namespace bsct

@@ -116,9 +116,10 @@ cudaError_t backproject_v3(int N, int n_angles, int M, int B, const BPAngle *ang
                            float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s);
 
 // K7 (forward.cu)
+// work: [B][N][N] scratch (transposed image); not read by the caller afterwards
 template <typename T>
 cudaError_t forward_project(int N, double lx, double ly, int n_angles, int M, int B, const double *cs,
-                            PPView<T> tb, const T *c, T *sino, cudaStream_t s);
+                            PPView<T> tb, const T *c, T *sino, cudaStream_t s, T *work);
 
 // K6 (solver.cu)
 struct SolverWork {

@@ -1,4 +1,4 @@
-"""Time K7 (forward projection) v2 vs v1 on config-5 geometry, 64 slices."""
+"""Time K7 (forward projection) v3 vs v1 on config-5 geometry, 64 slices."""
 import os, sys, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
@@ -15,7 +15,7 @@ for v in ("1", "0"):
     bsct.forward_project(plan, x, s); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(); bsct.forward_project(plan, x, s); e1.record(); torch.cuda.synchronize()
-    out["v1" if v == "1" else "v2"] = (e0.elapsed_time(e1), s.clone())
-d = float((out["v1"][1] - out["v2"][1]).norm() / out["v1"][1].norm())
-print(json.dumps({"v1_ms": out["v1"][0], "v2_ms": out["v2"][0], "rel_diff": d,
-                  "v2_gvox_angle_s": B * N * N * cfg.n_angles / (out["v2"][0] / 1e3) / 1e9}))
+    out["v1" if v == "1" else "v3"] = (e0.elapsed_time(e1), s.clone())
+d = float((out["v1"][1] - out["v3"][1]).norm() / out["v1"][1].norm())
+print(json.dumps({"v1_ms": out["v1"][0], "v3_ms": out["v3"][0], "rel_diff": d,
+                  "v3_gvox_angle_s": B * N * N * cfg.n_angles / (out["v3"][0] / 1e3) / 1e9}))
