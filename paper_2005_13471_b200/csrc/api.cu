@@ -386,6 +386,13 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     p->rho_iters = iters;
   }
   T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
+  if (!p->solver_v1 && onchip_enabled() && onchip_cluster_size(p->N, p->L, p->dt == BSCT_F32) > 0) {
+    // NEXT-2: small N -- one thread-block cluster per slice runs every iteration on chip
+    LAUNCH(p, BSCT_K_FUSED_CG, 1,
+           (onchip_solve<T>(p->N, p->L, B, iters, solver, b, x, r, pp, (const T *)p->S, (const cplx<T> *)p->tw,
+                            p->tau, resid, flags ? flags : p->flags, s)));
+    return BSCT_OK;
+  }
   if (!p->solver_v1) {
     // fused iteration (cg.cu): 3 launches per iteration.  Slices are solved in chunks whose
     // per-iteration working set (x, r, p, T1) stays resident in L2, so that the FFT

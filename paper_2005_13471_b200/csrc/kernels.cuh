@@ -150,6 +150,12 @@ struct FusedWork {
   double *tau;     // Landweber step (device)
 };
 int fused_parts(int N, int L, bool fp32);  // pass A / C CTAs per slice
+// NEXT-2 (onchip.cu): cluster-resident solver loop for small N (L <= 512); mode 0 CG, 1 SD, 2 Landweber
+bool onchip_enabled();                               // opt-in: BSCT_ONCHIP=1
+int onchip_cluster_size(int N, int L, bool fp32);    // 0: not supported
+template <typename T>
+cudaError_t onchip_solve(int N, int L, int B, int iters, int mode, const T *b, T *x, T *r, T *p, const T *S,
+                         const cplx<T> *tw, const double *tau, double *resid, int *flags, cudaStream_t s);
 // y = G x with the FP32 L = 1024 warp-FFT passes A and C (cudaErrorNotSupported otherwise)
 cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaStream_t s);
 cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaStream_t s);

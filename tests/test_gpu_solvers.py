@@ -203,3 +203,26 @@ def test_chebyshev(cuda_lib, ci, iters, tl):
     assert rel_l2(to_np(x2[0]), xr) < 10 * tl
     with pytest.raises(cuda_lib.BsctError):
         cuda_lib.chebyshev_solve(plan, to_dev(b, cfg.dtype), x2, iters, lmax * 2, lmax)
+
+
+@pytest.mark.parametrize("N,dt", [(1, "f32"), (16, "f64"), (64, "f64"), (100, "f32"), (128, "f32"), (200, "f32"),
+                                  (256, "f32"), (128, "f64")])
+@pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
+def test_onchip_cluster_solver(cuda_lib, N, dt, solver, monkeypatch):
+    """NEXT-2: the cluster-resident solver loop (onchip.cu, one thread-block cluster of 1-8 CTAs
+    per slice, T1 distributed over the CTAs' shared memory) against the fused multi-launch path
+    (BSCT_ONCHIP=0) and, for CG, the FP64 oracle; B = 3 with distinct right-hand sides."""
+    cfg = CONFIGS[2].with_(N=N, n_angles=48, n_det=2 * N + 3, ellipse_scale=max(N, 8) / 64, dtype=dt)
+    T = gram_taps(cfg.geometry())
+    b = rhs(cfg, T, B=3)
+    K = 6
+    monkeypatch.setenv("BSCT_ONCHIP", "1")
+    xo, ho = run(cuda_lib, cfg, b, K, solver, B=3)
+    monkeypatch.setenv("BSCT_ONCHIP", "0")
+    xf, hf = run(cuda_lib, cfg, b, K, solver, B=3)
+    tl = 1e-10 if dt == "f64" else (1e-4 if solver == "cg" else 1e-5)
+    assert rel_l2(xo, xf) < tl
+    assert rel_l2(ho, hf) < tl
+    if solver == "cg":
+        xr, _ = solvers.cg(T, b[2], K)
+        assert rel_l2(xo[2], xr) < (1e-9 if dt == "f64" else 1e-4)

@@ -5,11 +5,11 @@ O=gpurun_out/$T; mkdir -p $O
 python -m pytest tests -m gpu -q > $O/pytest_gpu.log 2>&1; echo "rc=$?" >> $O/pytest_gpu.log
 python bench.py > $O/bench.jsonl 2> $O/bench.err
 # launch list (cold-cache, serialised: compare shares) of a shorter bench command
-CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu"
+CMD="python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-cufft"
 $CMD > $O/plain_launch.log 2>&1 && \
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches.csv $CMD > $O/ncu_launch.log 2>&1
 echo "launch rc=$?"
 CMD2="python bench.py --slices 64 --iters 2 --steps 1 --warmup 1 --no-e2e --no-cpu"
 $CMD2 > $O/plain_full.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"bp_v3|pass_[abc]_1024|correction" -s 6 -c 5 -o $O/prof_full $CMD2 > $O/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"bp_v3|pass_[abc]_1024|correction|forward_v3" -s 6 -c 6 -o $O/prof_full $CMD2 > $O/ncu_full.log 2>&1
 echo "full rc=$?"

@@ -1,0 +1,40 @@
+"""NEXT-2 timing: cluster-resident solver loop vs the fused 3-launch iteration (config 2 and 1)."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+
+import paper_2005_13471_b200 as bsct
+from synth import CONFIGS
+
+out = []
+for ci, Bs in ((2, (1, 16, 128)), (1, (1, 64))):
+    cfg = CONFIGS[ci]
+    g = cfg.geometry()
+    N = cfg.N
+    dt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    taps = torch.empty((2 * N - 1, 2 * N - 1), device="cuda", dtype=dt)
+    bsct.gram_build(g, taps)
+    for B in Bs:
+        plan = bsct.plan_create(g, taps, max_batch=B)
+        b = torch.rand((B, N, N), device="cuda", dtype=dt)
+        x = torch.empty_like(b)
+        row = {"config": ci, "N": N, "B": B, "iters": cfg.iters, "dtype": cfg.dtype}
+        for mode in ("1", "0"):
+            os.environ["BSCT_ONCHIP"] = mode
+            bsct.cg_solve(plan, b, x, cfg.iters, "cg")
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(5):
+                bsct.cg_solve(plan, b, x, cfg.iters, "cg")
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / 5
+            row["onchip_ms" if mode == "1" else "fused_ms"] = ms
+        row["speedup"] = row["fused_ms"] / row["onchip_ms"]
+        row["onchip_slice_iter_s"] = B * cfg.iters / (row["onchip_ms"] / 1e3)
+        out.append(row)
+        print(json.dumps(row), flush=True)
