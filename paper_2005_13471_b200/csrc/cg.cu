@@ -23,6 +23,7 @@ namespace bsct {
 
 const float2 *tw1024_table();  // normal.cu: W_1024^{jt}, [32][32]
 bool pass_c_warp_enabled();
+bool bulk_stage_enabled();  // BSCT_BULK=1: bulk (TMA) copies instead of cp.async staging
 
 __device__ __forceinline__ double cta_sum(double v, double *red) {
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -402,7 +403,8 @@ template <int MODE, int ROWS>
 __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_c_1024_kernel(int N, int k, int gparts,
                                                                 const float2 *__restrict__ T1,
                                                                 float *__restrict__ x, float *__restrict__ r,
-                                                                const float2 *__restrict__ tw1024, FusedWork w) {
+                                                                const float2 *__restrict__ tw1024, FusedWork w,
+                                                                int use_bulk) {
   constexpr int L = 1024, Q = L / 2 + 1, NW = ROWS / 2, RS = NW + 1;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] row pairs, later [NW][32][33] float2
@@ -411,9 +413,31 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_c_1024_kernel(in
   const int b = blockIdx.y;
   const int row0 = blockIdx.x * ROWS;
   const int rows = min(ROWS, N - row0);
-  // stage T1[q][row0 .. row0 + ROWS) asynchronously; rows beyond N are zero
+  // stage T1[q][row0 .. row0 + ROWS) asynchronously; rows beyond N are zero.  N even: one bulk
+  // (TMA) copy per q of the rows' contiguous 8 * rows bytes, completion counted on an mbarrier;
+  // N odd: 8-byte cp.async per entry
   const float2 *T1s = T1 + (size_t)b * Q * N + row0;
-  for (int i = threadIdx.x; i < Q * NW; i += blockDim.x) {
+  __shared__ __align__(8) unsigned long long stage_bar;
+  const bool bulk = !(N & 1) && use_bulk;
+  const unsigned bar = (unsigned)__cvta_generic_to_shared(&stage_bar);
+  if (bulk) {
+    if (threadIdx.x == 0) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(bar));
+      asm volatile("fence.mbarrier_init.release.cluster;\n" ::);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bar), "r"(Q * rows * 8));
+    }
+    __syncthreads();
+    for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+      float4 *dst = st + q * RS;
+      const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(d),
+          "l"(T1s + (size_t)q * N), "r"(rows * 8), "r"(bar)
+          : "memory");
+      for (int pr = rows / 2; pr < NW; ++pr) dst[pr] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  for (int i = threadIdx.x; i < (bulk ? 0 : Q * NW); i += blockDim.x) {
     const int q = i / NW, pr = i % NW, rp = 2 * pr;
     float4 *dst = st + q * RS + pr;
     const float2 *src = T1s + (size_t)q * N + rp;
@@ -458,6 +482,15 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_c_1024_kernel(in
   if (MODE != 3 && blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
   const float al = (float)alpha;
   asm volatile("cp.async.wait_group 0;\n" ::);
+  if (bulk) {  // phase 0 of the staging barrier: every byte of the tile has landed
+    unsigned done = 0;
+    while (!done)
+      asm volatile(
+          "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n selp.u32 %0, 1, 0, p;\n}\n"
+          : "=r"(done)
+          : "r"(bar)
+          : "memory");
+  }
   __syncthreads();
   // row pair (2 warp, 2 warp + 1): Z[q] = X_a[q] + i X_b[q], Z[L - q] = conj X_a[q] + i conj X_b[q]
   float2 v[32];
@@ -589,6 +622,14 @@ static bool can_vec(int N, const void *a, const void *b, const void *c) {
   return N % VW == 0 && al(a) && al(b) && al(c);
 }
 
+// Bulk (TMA, cp.async.bulk) staging of pass C's T1 tile: opt-in (BSCT_BULK=1).  Measured on B200,
+// config 5: 117 ms per step vs 97 ms with 16-byte cp.async -- one 128-byte bulk copy per q is too
+// small for the bulk-copy path to pay off.
+bool bulk_stage_enabled() {
+  const char *e = getenv("BSCT_BULK");
+  return e && e[0] == '1';
+}
+
 bool pass_c_warp_enabled() {
   const char *e = getenv("BSCT_PASSC_V1");  // read per call: tests switch it within one process
   return !(e && e[0] == '1');
@@ -647,7 +688,8 @@ static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *
       constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * (WROWS / 2 + 1);
       cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<MODE, WROWS>, sm);
       if (e != cudaSuccess) return e;
-      cg_pass_c_1024_kernel<MODE, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, gparts, T1, x, r, twl, w);
+      cg_pass_c_1024_kernel<MODE, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, gparts, T1, x, r, twl, w,
+                                                                                   bulk_stage_enabled());
       return cudaGetLastError();
     }
   }
@@ -737,7 +779,8 @@ cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaSt
   w.B = B;
   cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<3, WROWS>, sm);
   if (e != cudaSuccess) return e;
-  cg_pass_c_1024_kernel<3, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w);
+  cg_pass_c_1024_kernel<3, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w,
+                                                                             bulk_stage_enabled());
   return cudaGetLastError();
 }
 

@@ -226,3 +226,15 @@ def test_onchip_cluster_solver(cuda_lib, N, dt, solver, monkeypatch):
     if solver == "cg":
         xr, _ = solvers.cg(T, b[2], K)
         assert rel_l2(xo[2], xr) < (1e-9 if dt == "f64" else 1e-4)
+
+
+def test_bulk_staging_equals_cp_async(cuda_lib, monkeypatch):
+    """Pass C's T1 tile staged by bulk (TMA) copies (BSCT_BULK=1) equals the cp.async staging."""
+    cfg = CONFIGS[3].with_(N=512, n_angles=60, n_det=725, ellipse_scale=8.0)
+    T = gram_taps(cfg.geometry())
+    b = rhs(cfg, T, B=2)
+    monkeypatch.setenv("BSCT_BULK", "1")
+    xb, hb = run(cuda_lib, cfg, b, 4, "cg", B=2)
+    monkeypatch.setenv("BSCT_BULK", "0")
+    xc, hc = run(cuda_lib, cfg, b, 4, "cg", B=2)
+    assert np.array_equal(xb, xc) and np.array_equal(hb, hc)
