@@ -72,3 +72,25 @@ def test_validation_without_device(lib):
     assert lib.bsct_gram_build(ctypes.byref(s), bsct.F32, 0, 4, None, None) == bsct.EINVAL
     assert lib.bsct_plan_destroy(None) == bsct.OK
     assert lib.bsct_backproject(None, None, None, 1, None) == bsct.EINVAL
+
+
+def test_null_plan_rejected_everywhere(lib):
+    """Every plan-taking entry point rejects a NULL plan with BSCT_EINVAL (no device work)."""
+    import paper_2005_13471_b200 as bsct
+    vp = ctypes.c_void_p
+    calls = [
+        lambda: lib.bsct_correction_filter(None, vp(1), vp(1), 1, None),
+        lambda: lib.bsct_normal_apply(None, vp(1), vp(1), 1, None),
+        lambda: lib.bsct_cg_solve(None, vp(1), vp(1), 1, 3, 0, None, None, None),
+        lambda: lib.bsct_forward_project(None, vp(1), vp(1), 1, None),
+        lambda: lib.bsct_reconstruct(None, vp(1), vp(1), 1, 3, 0, None, None, None),
+        lambda: lib.bsct_reconstruct_host(None, vp(1), vp(1), 1, 3, 0, None),
+        lambda: lib.bsct_adjoint_project(None, vp(1), vp(1), 1, None),
+        lambda: lib.bsct_sirt_solve(None, vp(1), vp(1), 1, 3, None),
+        lambda: lib.bsct_chebyshev_solve(None, vp(1), vp(1), 1, 3, 0.1, 1.0, None, None),
+        lambda: lib.bsct_plan_set_filter(None, vp(1), None),
+        lambda: lib.bsct_plan_profile(None, 1),
+    ]
+    for c in calls:
+        assert c() == bsct.EINVAL
+        assert b"plan" in lib.bsct_last_error()
