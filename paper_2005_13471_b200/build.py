@@ -73,6 +73,14 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
 
     with ThreadPoolExecutor(max_workers=jobs or os.cpu_count() or 4) as ex:
         done = [d for d in ex.map(compile_one, zip(srcs, objs)) if d]
+    # drop cached objects of older source versions (the cache otherwise grows without bound)
+    keep = set(os.path.basename(o) for o in objs) | {"libbsct.stamp"}
+    for f in os.listdir(BUILD):
+        if f not in keep and (f.endswith(".o") or f.endswith(".tmp")):
+            try:
+                os.remove(os.path.join(BUILD, f))
+            except OSError:
+                pass
     stamp = os.path.join(BUILD, "libbsct.stamp")
     key = "\n".join(objs)
     if done or force or not os.path.exists(LIB) or not os.path.exists(stamp) or open(stamp).read() != key:

@@ -193,25 +193,32 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(in
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int b = blockIdx.y;
-  // PLAIN (y = G x): p is the input x, nothing is updated
-  const double rho = PLAIN ? 0.0 : cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
-  double beta = 0.0, alpha_prev = 0.0;
-  if (!PLAIN && k > 0) {
-    const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
-    beta = rho_prev > 0 ? rho / rho_prev : 0.0;
-    alpha_prev = w.alpha[b];
-  }
-  if (!PLAIN && blockIdx.x == 0 && threadIdx.x == 0) {
-    w.rho[(size_t)b * w.rho_stride + k] = rho;
-    if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
-  }
-  const float be = (float)beta, al = (float)alpha_prev;
+  // PLAIN (y = G x): p is the input x, nothing is updated.  The scalars (rho_k from the <r, r>
+  // partials, beta, alpha_{k-1}) are formed after the first batch of row loads is in flight.
+  float be = 0.f, al = 0.f;
+  auto scalars = [&]() {
+    if (PLAIN) return;
+    const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    double beta = 0.0, alpha_prev = 0.0;
+    if (k > 0) {
+      const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
+      beta = rho_prev > 0 ? rho / rho_prev : 0.0;
+      alpha_prev = w.alpha[b];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+    be = (float)beta;
+    al = (float)alpha_prev;
+  };
   const int row0 = blockIdx.x * ROWS;
   const int rows = min(ROWS, N - row0);
   const size_t so = (size_t)b * N * N + (size_t)row0 * N;
   // streaming phase (VW-wide): x += a p_old, p = r + b p_old; p rows -> ps, zero-padded to PW
   // batches of UB items per thread: all 3 UB loads are issued before the first use
   constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
+  static_assert(ITEMS % (UB * NT) == 0, "every thread runs the same number of batches (the first one reduces)");
   for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
     float pv[UB][VW], rv[UB][VW], xv[UB][VW];
     bool ok[UB];
@@ -229,6 +236,7 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(in
         }
       }
     }
+    if (i0 == (int)threadIdx.x) scalars();  // first batch: uniform across the CTA
 #pragma unroll
     for (int u = 0; u < UB; ++u) {
       const int i = i0 + u * NT;
