@@ -86,12 +86,15 @@ __global__ void __launch_bounds__(256) transpose_kernel(int N, const T *__restri
     if (x0 + r < N && y0 + threadIdx.x < N) dst[(size_t)(x0 + r) * N + y0 + threadIdx.x] = t[threadIdx.x][r];
 }
 
-template <typename T, int PC>
-__global__ void __launch_bounds__(256) forward_v3_kernel(int N, double lx, double ly, int n_angles, int M,
+// SB slices per CTA: the weight M(arg) of a (sample, pixel) pair is the same for every slice,
+// so each evaluation serves SB pixel loads and FMAs.
+template <typename T, int PC, int SB>
+__global__ void __launch_bounds__(256) forward_v3_kernel(int N, int B, double lx, double ly, int n_angles, int M,
                                                          const double *__restrict__ cs, PPView<T> tb,
                                                          const T *__restrict__ c, const T *__restrict__ ct,
                                                          T *__restrict__ sino) {
-  const int a = blockIdx.x, b = blockIdx.y;
+  const int a = blockIdx.x, b0 = blockIdx.y * SB;
+  const int nb = min(SB, B - b0);
   __shared__ T kn_s[FWD_MAXP + 1], cf_s[FWD_MAXP][3];
   __shared__ int nw_s;
   const int np = tb.npieces[a];
@@ -120,7 +123,8 @@ __global__ void __launch_bounds__(256) forward_v3_kernel(int N, double lx, doubl
     return fma(fma(cf_s[j][2], t, cf_s[j][1]), t, cf_s[j][0]);
   };
   const bool rows = fabs(co) >= fabs(si);
-  const T *img = (rows ? c : ct) + (size_t)b * N * N;  // line l = row l of img, pixels j along it
+  const T *img = (rows ? c : ct) + (size_t)b0 * N * N;  // line l = row l of img, pixels j along it
+  const size_t NN = (size_t)N * N;
   const int h = N / 2;
   // arg(l, j) = A(l) - st j;  A(l) = A0 + l dA  (rows: kt = -si x1 + co x2 with x1 = lx (l - h),
   // x2 = lx (j - h); columns: x2 = lx (l - h), x1 = lx (j - h))
@@ -151,7 +155,9 @@ __global__ void __launch_bounds__(256) forward_v3_kernel(int N, double lx, doubl
     } else if (!(e00 < N && e00 + w > -1.0)) {
       l1 = -1;
     }
-    T acc = 0;
+    T acc[SB];
+#pragma unroll
+    for (int sl = 0; sl < SB; ++sl) acc[sl] = 0;
     double elo = e00 + (double)l0 * de;
     for (int l = l0; l <= l1; ++l, elo += de) {
       const double t0 = (elo - 0.5) + FWD_MAGIC;
@@ -170,10 +176,15 @@ __global__ void __launch_bounds__(256) forward_v3_kernel(int N, double lx, doubl
         const T v = nw == 1 ? box : fma(fma(cf_s[q][2], tq, cf_s[q][1]), tq, cf_s[q][0]);
         const bool sup = nw == 1 ? (arg >= -Ht && arg < Ht) : (ax < Ht);
         const bool in = sup && (unsigned)j < (unsigned)N;
-        if (in) acc = fma(line[j], v, acc);
+        if (in)
+#pragma unroll
+          for (int sl = 0; sl < SB; ++sl)
+            if (sl < nb) acc[sl] = fma(line[sl * NN + j], v, acc[sl]);
       }
     }
-    sino[((size_t)b * n_angles + a) * M + m] = (T)(lx * lx) * acc;
+#pragma unroll
+    for (int sl = 0; sl < SB; ++sl)
+      if (sl < nb) sino[((size_t)(b0 + sl) * n_angles + a) * M + m] = (T)(lx * lx) * acc[sl];
   }
 }
 
@@ -188,7 +199,9 @@ cudaError_t forward_project(int N, double lx, double ly, int n_angles, int M, in
     if (!work) return cudaErrorInvalidValue;  // [B][N][N] scratch for the transposed image
     transpose_kernel<T><<<dim3((N + 31) / 32, (N + 31) / 32, B), dim3(32, 8), 0, s>>>(N, c, work);
     // the forward model's box spline has <= 3 widths: <= 5 right-half pieces, 4 knot compares
-    forward_v3_kernel<T, 4><<<dim3(n_angles, B), 256, 0, s>>>(N, lx, ly, n_angles, M, cs, tb, c, work, sino);
+    constexpr int FSB = 8;  // slices per CTA (measured: 4 -> 339, 8 -> 356 Gvox-angle/s at config 5)
+    forward_v3_kernel<T, 4, FSB><<<dim3(n_angles, (B + FSB - 1) / FSB), 256, 0, s>>>(N, B, lx, ly, n_angles, M, cs,
+                                                                                  tb, c, work, sino);
   }
   return cudaGetLastError();
 }
