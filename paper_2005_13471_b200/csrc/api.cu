@@ -465,7 +465,7 @@ bsct_status adjoint_core(bsct_plan p, const T *gt, T *out, int B, cudaStream_t s
   if (sb > 0)
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject_v3(p->N, p->n_angles, p->M, B, p->adj_ang, (const float *)p->adj_B, (const float *)gt,
-                           (float *)out, p->bp_cells, p->bp_maxp, scale, sb, s)));
+                           (float *)out, p->bp_cells, p->bp_maxp, scale, sb, s, 3)));
   else
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject_v2<T>(p->N, p->n_angles, p->M, B, p->adj_ang, (const T *)p->adj_B, gt, out, p->bp_cells,

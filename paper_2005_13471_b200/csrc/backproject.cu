@@ -534,13 +534,15 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // wavefronts per load on average over the config-5 angles (vs ~7.4 per 16-byte load for
 // 32-pixel rows with 32-byte entries; bank model checked against ncu).  The sub-interval
 // start bp_p is selected from registers alongside the sub-interval search.
-template <int SB, int PC, int PL>
+// NC: polynomial coefficients per entry -- 6 for the back projection's degree-5 kernel, 3 for
+// the plain adjoint's (forward model, <= 3 widths: degree <= 2; half the table traffic)
+template <int SB, int PC, int PL, int NC>
 __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int n_angles, int M,
                                                               const BPAngle *__restrict__ ang,
                                                               const float *__restrict__ Btab,
                                                               const float *__restrict__ gt, float *__restrict__ out,
                                                               int max_cells, int maxP, float scale) {
-  constexpr int TAB = SB * 6 * PL;  // floats per table buffer
+  constexpr int TAB = SB * NC * PL;  // floats per table buffer
   extern __shared__ __align__(16) unsigned char smem_raw[];
   float *sm = reinterpret_cast<float *>(smem_raw);
   const int bst_sz = maxP * BP_SMAX * 8;
@@ -596,11 +598,11 @@ __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int 
     // build F_s[c][p][k] = sum_i g~_s[c + i + imin] B[p][i][k] for the tile's cells, all SB slices
     for (int item = threadIdx.x; item < P * ta.ncell; item += BP_THREADS) {
       const int p = item / ta.ncell, cc = item - p * ta.ncell;
-      float f[SB][6];
+      float f[SB][NC];
 #pragma unroll
       for (int sl = 0; sl < SB; ++sl)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) f[sl][k] = 0.f;
+        for (int k = 0; k < NC; ++k) f[sl][k] = 0.f;
       const float *Bp = Bst + p * BP_SMAX * 8;
       for (int i = 0; i < S; ++i) {
         float bb[8];
@@ -609,14 +611,14 @@ __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int 
         for (int sl = 0; sl < SB; ++sl) {
           const float gv = gst[sl * gseg + cc + i];
 #pragma unroll
-          for (int k = 0; k < 6; ++k) f[sl][k] = fmaf(gv, bb[k], f[sl][k]);
+          for (int k = 0; k < NC; ++k) f[sl][k] = fmaf(gv, bb[k], f[sl][k]);
         }
       }
       float *dst = tab + cc * P + p;
 #pragma unroll
       for (int sl = 0; sl < SB; ++sl)
 #pragma unroll
-        for (int k = 0; k < 6; ++k) dst[(sl * 6 + k) * PL] = f[sl][k];
+        for (int k = 0; k < NC; ++k) dst[(sl * NC + k) * PL] = f[sl][k];
     }
     // slot (a + 2) % 3 was last read by build(a - 1), before the previous barrier
     stage(a + 2);
@@ -649,12 +651,9 @@ __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int 
       const float *e = tb + ci * P + po;
 #pragma unroll
       for (int sl = 0; sl < SB; ++sl) {
-        float rr = e[(sl * 6 + 5) * PL];
-        rr = fmaf(rr, tau, e[(sl * 6 + 4) * PL]);
-        rr = fmaf(rr, tau, e[(sl * 6 + 3) * PL]);
-        rr = fmaf(rr, tau, e[(sl * 6 + 2) * PL]);
-        rr = fmaf(rr, tau, e[(sl * 6 + 1) * PL]);
-        rr = fmaf(rr, tau, e[(sl * 6 + 0) * PL]);
+        float rr = e[(sl * NC + NC - 1) * PL];
+#pragma unroll
+        for (int k = NC - 2; k >= 0; --k) rr = fmaf(rr, tau, e[(sl * NC + k) * PL]);
         acc[sl][j] += rr;
       }
     }
@@ -676,21 +675,21 @@ static int bp_v3_plane(int max_cells, int maxP) {
   return need <= 512 ? 512 : need <= 1024 ? 1024 : need <= 2048 ? 2048 : 0;
 }
 
-static size_t bp_v3_smem(int SB, int max_cells, int maxP) {
+static size_t bp_v3_smem(int SB, int max_cells, int maxP, int NC = 6) {
   const size_t PL = (size_t)bp_v3_plane(max_cells, maxP);
   const size_t stg = (size_t)maxP * BP_SMAX * 8 + SB * (size_t)((max_cells + BP_SMAX + 3) & ~3);
-  return sizeof(float) * (2 * (size_t)SB * 6 * PL + 3 * stg);
+  return sizeof(float) * (2 * (size_t)SB * NC * PL + 3 * stg);
 }
 
-template <int SB, int PC, int PL>
+template <int SB, int PC, int PL, int NC>
 static cudaError_t launch_bp_v3(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab,
                                 const float *gt, float *b, int max_cells, int maxP, float scale, cudaStream_t s) {
-  const size_t sm = bp_v3_smem(SB, max_cells, maxP);
+  const size_t sm = bp_v3_smem(SB, max_cells, maxP, NC);
   if (sm > 227 * 1024 || max_cells * maxP > PL) return cudaErrorInvalidConfiguration;
-  cudaError_t e = cudaFuncSetAttribute(bp_v3_kernel<SB, PC, PL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  cudaError_t e = cudaFuncSetAttribute(bp_v3_kernel<SB, PC, PL, NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   dim3 grid((N + BPT - 1) / BPT, (N + BPT - 1) / BPT, (B + SB - 1) / SB);
-  bp_v3_kernel<SB, PC, PL><<<grid, BP_THREADS, sm, s>>>(N, B, n_angles, M, ang, Btab, gt, b, max_cells, maxP, scale);
+  bp_v3_kernel<SB, PC, PL, NC><<<grid, BP_THREADS, sm, s>>>(N, B, n_angles, M, ang, Btab, gt, b, max_cells, maxP, scale);
   return cudaGetLastError();
 }
 
@@ -706,12 +705,15 @@ int bp_v3_slices(int B, int maxP, int max_cells) {
 }
 
 cudaError_t backproject_v3(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
-                           float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s) {
+                           float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s, int ncoef) {
   const float sc = (float)scale;
   const int PL = bp_v3_plane(max_cells, maxP);
-#define BP3(SBV, PLV)                                                                                         \
-  return maxP <= 5 ? launch_bp_v3<SBV, 4, PLV>(N, n_angles, M, B, ang, Btab, gt, b, max_cells, maxP, sc, s) \
-                   : launch_bp_v3<SBV, 8, PLV>(N, n_angles, M, B, ang, Btab, gt, b, max_cells, maxP, sc, s)
+#define BP3N(SBV, PLV, NCV)                                                                                     \
+  return maxP <= 5 ? launch_bp_v3<SBV, 4, PLV, NCV>(N, n_angles, M, B, ang, Btab, gt, b, max_cells, maxP, sc, s) \
+                   : launch_bp_v3<SBV, 8, PLV, NCV>(N, n_angles, M, B, ang, Btab, gt, b, max_cells, maxP, sc, s)
+#define BP3(SBV, PLV)                 \
+  if (ncoef == 3) { BP3N(SBV, PLV, 3); } \
+  BP3N(SBV, PLV, 6)
 #define BP3P(SBV)                        \
   switch (PL) {                          \
     case 512: BP3(SBV, 512);             \
@@ -724,6 +726,7 @@ cudaError_t backproject_v3(int N, int n_angles, int M, int B, const BPAngle *ang
   BP3P(1);
 #undef BP3P
 #undef BP3
+#undef BP3N
 }
 
 // Host replica of the breakpoint count of bp_tables_kernel (sizes the shared memory; merges

@@ -112,8 +112,9 @@ cudaError_t backproject_v2(int N, int n_angles, int M, int B, const BPAngle *ang
 
 // K4 v3 (FP32): SB in {1, 2, 4} slices per CTA share each pixel's locate
 int bp_v3_slices(int B, int maxP, int max_cells);
+// ncoef: 6 (back projection, degree 5) or 3 (plain adjoint, degree <= 2)
 cudaError_t backproject_v3(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
-                           float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s);
+                           float *b, int max_cells, int maxP, double scale, int SB, cudaStream_t s, int ncoef = 6);
 
 // K7 (forward.cu)
 // work: [B][N][N] scratch (transposed image); not read by the caller afterwards
