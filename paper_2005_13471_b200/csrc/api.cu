@@ -66,6 +66,12 @@ size_t tables_bytes(int n) { return PPTables<T>::bytes(n); }
 
 }  // namespace
 
+struct GraphEntry {  // a captured solve: argument key -> instantiated graph
+  const void *key[8];
+  cudaGraphExec_t exec;
+  int64_t launches;
+};
+
 struct bsct_plan_s {
   int N = 0, L = 0, n_angles = 0, M = 0, max_batch = 0;
   double lx = 1, ly = 1, zeta = 0;
@@ -92,6 +98,8 @@ struct bsct_plan_s {
   int64_t launches = 0;
   // reconstruct pipeline: aux streams (BP / H2D, D2H) and per-chunk events
   cudaStream_t aux = nullptr, aux2 = nullptr, hi = nullptr;  // hi: solves, highest priority
+  cudaStream_t cap = nullptr;                                  // graph capture of small solves
+  std::vector<GraphEntry> graphs;
   std::vector<cudaEvent_t> pipe_ev;
   // kernel-class profiler: CUDA events bracket every launch on the caller's stream
   bool prof_on = false;
@@ -377,6 +385,19 @@ int solver_chunk(bsct_plan p, int B) {
 }
 
 template <typename T>
+bsct_status solve_launch_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver, double *resid, int *flags,
+                           cudaStream_t s);
+
+bsct_status clear_graphs(bsct_plan p) {
+  for (auto &gk : p->graphs) cudaGraphExecDestroy(gk.exec);
+  p->graphs.clear();
+  return BSCT_OK;
+}
+
+// Small problems (B N^2 <= 2^22 values, profiler off) are launch bound: the whole solve (init,
+// 3 launches per iteration, finish) is captured once per argument set into a CUDA graph on a
+// plan-owned stream and replayed on the caller's stream (BSCT_GRAPH=0: plain launches).
+template <typename T>
 bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver, double *resid, int *flags,
                     cudaStream_t s) {
   if (p->rho_iters < iters) {
@@ -384,7 +405,55 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     p->rho = nullptr;
     CU(cudaMalloc((void **)&p->rho, sizeof(double) * (size_t)(iters + 1) * (p->max_batch > 0 ? p->max_batch : 1)));
     p->rho_iters = iters;
+    clear_graphs(p);  // captured graphs hold the old rho pointer
   }
+  const char *ge = getenv("BSCT_GRAPH");
+  const bool graph = !(ge && ge[0] == '0') && !p->prof_on && (size_t)B * p->N * p->N <= ((size_t)1 << 22);
+  if (!graph) return solve_launch_t<T>(p, b, x, B, iters, solver, resid, flags, s);
+  // the key includes every switch that selects the launched code path
+  const intptr_t path = (onchip_enabled() ? 1 : 0) | (pass_b_warp_enabled() ? 2 : 0) | (pass_c_warp_enabled() ? 4 : 0) |
+                        (bulk_stage_enabled() ? 8 : 0) | (p->solver_v1 ? 16 : 0) |
+                        ((intptr_t)solver_chunk(p, B) << 8);
+  const void *key[8] = {b, x, (const void *)(intptr_t)B, (const void *)(intptr_t)iters,
+                        (const void *)(intptr_t)solver, resid, flags, (const void *)path};
+  for (auto &gk : p->graphs)
+    if (std::equal(key, key + 8, gk.key)) {
+      CU(cudaGraphLaunch(gk.exec, s));
+      p->launches = gk.launches;
+      return BSCT_OK;
+    }
+  if (!p->cap) CU(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
+  (void)tw1024_table();  // any lazy device allocation happens before capture
+  CU(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
+  p->launches = 0;
+  bsct_status st = solve_launch_t<T>(p, b, x, B, iters, solver, resid, flags, p->cap);
+  cudaGraph_t g = nullptr;
+  cudaError_t e = cudaStreamEndCapture(p->cap, &g);
+  if (st != BSCT_OK) {
+    if (g) cudaGraphDestroy(g);
+    return st;
+  }
+  CU(e);
+  cudaGraphExec_t ex = nullptr;
+  e = cudaGraphInstantiate(&ex, g, 0);
+  cudaGraphDestroy(g);
+  CU(e);
+  if (p->graphs.size() >= 16) {
+    cudaGraphExecDestroy(p->graphs.front().exec);
+    p->graphs.erase(p->graphs.begin());
+  }
+  GraphEntry gk;
+  std::copy(key, key + 8, gk.key);
+  gk.exec = ex;
+  gk.launches = p->launches;
+  p->graphs.push_back(gk);
+  CU(cudaGraphLaunch(ex, s));
+  return BSCT_OK;
+}
+
+template <typename T>
+bsct_status solve_launch_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver, double *resid, int *flags,
+                           cudaStream_t s) {
   T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
   if (!p->solver_v1 && onchip_enabled() && onchip_cluster_size(p->N, p->L, p->dt == BSCT_F32) > 0) {
     // NEXT-2: small N -- one thread-block cluster per slice runs every iteration on chip
@@ -676,6 +745,8 @@ bsct_status bsct_plan_destroy(bsct_plan p) {
   if (p->aux) cudaStreamDestroy(p->aux);
   if (p->aux2) cudaStreamDestroy(p->aux2);
   if (p->hi) cudaStreamDestroy(p->hi);
+  for (auto &gk : p->graphs) cudaGraphExecDestroy(gk.exec);
+  if (p->cap) cudaStreamDestroy(p->cap);
   delete p;
   return BSCT_OK;
 }

@@ -238,3 +238,29 @@ def test_bulk_staging_equals_cp_async(cuda_lib, monkeypatch):
     monkeypatch.setenv("BSCT_BULK", "0")
     xc, hc = run(cuda_lib, cfg, b, 4, "cg", B=2)
     assert np.array_equal(xb, xc) and np.array_equal(hb, hc)
+
+
+@pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
+def test_graph_replay_equals_launches(cuda_lib, solver, monkeypatch):
+    """Small solves are captured into a CUDA graph and replayed (api.cu solve_t): bitwise equal
+    to plain launches, on first capture and on replay with new data in the same buffers."""
+    import torch
+    cfg = CONFIGS[2].with_(N=64, n_angles=40, n_det=131, ellipse_scale=1.0)
+    g = cfg.geometry()
+    T = gram_taps(g)
+    b = rhs(cfg, T, B=2)
+    plan, taps = gpu_plan(cuda_lib, g, "f32", max_batch=2)
+    bd = to_dev(b, "f32")
+    xs = []
+    for mode in ("1", "1", "0"):  # capture, replay, plain launches
+        monkeypatch.setenv("BSCT_GRAPH", mode)
+        x = torch.zeros((2, 64, 64), device="cuda") if not xs else xs[0][0]
+        h = torch.zeros((2, 7), dtype=torch.float64, device="cuda") if not xs else xs[0][1]
+        cuda_lib.cg_solve(plan, bd, x, 7, solver, resid_hist=h)
+        torch.cuda.synchronize()
+        xs.append((x, h, x.clone(), h.clone()))
+        bd.mul_(1.0)  # same data, same buffers
+    assert torch.equal(xs[0][2], xs[1][2]) and torch.equal(xs[0][3], xs[1][3])
+    assert torch.equal(xs[0][2], xs[2][2]) and torch.equal(xs[0][3], xs[2][3])
+    xr, _ = {"cg": solvers.cg, "sd": solvers.sd, "landweber": solvers.landweber}[solver](T, b[1], 7)
+    assert rel_l2(xs[0][2].double().cpu().numpy()[1], xr) < 1e-4

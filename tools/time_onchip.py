@@ -1,4 +1,5 @@
-"""NEXT-2 timing: cluster-resident solver loop vs the fused 3-launch iteration (config 2 and 1)."""
+"""Small-problem solve timing (configs 2 and 1): fused 3-launch iteration with / without CUDA-graph
+replay, and the NEXT-2 cluster-resident loop (onchip.cu)."""
 import json
 import os
 import sys
@@ -22,8 +23,9 @@ for ci, Bs in ((2, (1, 16, 128)), (1, (1, 64))):
         b = torch.rand((B, N, N), device="cuda", dtype=dt)
         x = torch.empty_like(b)
         row = {"config": ci, "N": N, "B": B, "iters": cfg.iters, "dtype": cfg.dtype}
-        for mode in ("1", "0"):
-            os.environ["BSCT_ONCHIP"] = mode
+        for mode, onchip, graph in (("onchip_ms", "1", "1"), ("fused_ms", "0", "1"), ("fused_nograph_ms", "0", "0")):
+            os.environ["BSCT_ONCHIP"] = onchip
+            os.environ["BSCT_GRAPH"] = graph
             bsct.cg_solve(plan, b, x, cfg.iters, "cg")
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -33,8 +35,8 @@ for ci, Bs in ((2, (1, 16, 128)), (1, (1, 64))):
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / 5
-            row["onchip_ms" if mode == "1" else "fused_ms"] = ms
-        row["speedup"] = row["fused_ms"] / row["onchip_ms"]
+            row[mode] = ms
+        row["graph_speedup"] = row["fused_nograph_ms"] / row["fused_ms"]
         row["onchip_slice_iter_s"] = B * cfg.iters / (row["onchip_ms"] / 1e3)
         out.append(row)
         print(json.dumps(row), flush=True)
