@@ -365,12 +365,18 @@ def run_ours(args):
         flops = vox_angles * (w_mean / cfg.lambda_y * 12.0 + 4.0)
         ms_launch = per[dom][0] / max(per[dom][1], 1)
         ach = flops / (ms_launch / 1e3) / 1e12
-        peak = fp32_peak_tflops(clk.get("sm_max_mhz") or 1965.0)
+        peak, peak_src = fp32_peak_tflops(clk.get("sm_max_mhz") or 1965.0), \
+            "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md)"
+        import glob
+        fm = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "fma_peak.json")))
+        if fm:  # measured on this pool's B200 by tools/fma_peak.cu
+            peak = float(json.load(open(fm[-1]))["fp32_fma_tflops"])
+            peak_src = f"measured: {os.path.relpath(fm[-1], ROOT)} (tools/fma_peak.cu, FP32 FMA chains)"
         tb, tsrc = ncu_traffic("bp_v3_kernel", B)
         roof = {"kernel": "backproject (K4)", "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
                 "frac": ach / peak, "traffic": tb, "traffic_source": tsrc,
                 "algorithmic_bytes": B * 4 * (n_ang * (M + 50) + N * N),
-                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md)",
+                "peak_source": peak_src,
                 "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6); "
                         "K4 v3 evaluates it from per-tile tables and is shared-memory bound (ncu L1/smem 81%)"}
     else:
