@@ -62,3 +62,39 @@ def test_config5_full_batch(cuda_lib):
     bs = to_np(b[0])
     xk, _ = solvers.cg(T, bs, int(np.ceil(0.8 * K)))
     assert solvers.objective(T, bs, to_np(x[0])) <= solvers.objective(T, bs, xk)
+
+
+def test_maximum_size_N2048(cuda_lib):
+    """Largest supported FP32 slice (N = 2048: L = 4096 generic FFT passes; K4 v3 over 32 x 32
+    tiles): taps, back projection (sampled pixels), normal apply (against the oracle's FFT
+    apply), 2 CG iterations; then empty batches through every call (no-ops)."""
+    import torch
+    from oracle.gram import gram_taps
+    from oracle.normal import apply_fft
+    N, n, M = 2048, 16, 2 * 2048 + 1
+    g = dict(N=N, lambda_x=1.0, angles=np.arange(n) * np.pi / n + 0.01, lambda_y=1.0, n_det=M, zeta=1.0)
+    taps = torch.empty((2 * N - 1, 2 * N - 1), device="cuda")
+    cuda_lib.gram_build(g, taps)
+    T = gram_taps(g)
+    assert rel_l2(to_np(taps), T) < 1e-5
+    plan = cuda_lib.plan_create(g, taps, max_batch=1)
+    assert plan.L == 4096
+    rng = np.random.default_rng(2048)
+    sino = rng.uniform(0, 1, (1, n, M))
+    b = torch.empty((1, N, N), device="cuda")
+    cuda_lib.backproject(plan, to_dev(sino, "f32"), b)
+    k1, k2 = rng.integers(0, N, 100), rng.integers(0, N, 100)
+    assert rel_l2(to_np(b[0])[k1, k2], backproject(g, sino[0], pixels=(k1, k2))) < 1e-5
+    x = to_dev(rng.uniform(-1, 1, (1, N, N)), "f32")
+    y = torch.empty_like(x)
+    cuda_lib.normal_apply(plan, x, y)
+    ref = apply_fft(T, to_np(x[0]))
+    assert rel_l2(to_np(y[0]), ref) < 1e-5
+    xs = torch.empty_like(b)
+    cuda_lib.cg_solve(plan, b, xs, 2, "cg")
+    xr, _ = solvers.cg(T, to_np(b[0]), 2)
+    assert rel_l2(to_np(xs[0]), xr) < 1e-4
+    # empty batch: every call is a no-op
+    cuda_lib.backproject(plan, to_dev(sino[:0], "f32"), b[:0])
+    cuda_lib.cg_solve(plan, b[:0], xs[:0], 2, "cg")
+    cuda_lib.reconstruct(plan, to_dev(sino[:0], "f32"), xs[:0], 2, "cg")
