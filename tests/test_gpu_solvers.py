@@ -263,4 +263,5 @@ def test_graph_replay_equals_launches(cuda_lib, solver, monkeypatch):
     assert torch.equal(xs[0][2], xs[1][2]) and torch.equal(xs[0][3], xs[1][3])
     assert torch.equal(xs[0][2], xs[2][2]) and torch.equal(xs[0][3], xs[2][3])
     xr, _ = {"cg": solvers.cg, "sd": solvers.sd, "landweber": solvers.landweber}[solver](T, b[1], 7)
-    assert rel_l2(xs[0][2].double().cpu().numpy()[1], xr) < 1e-4
+    # FP32 CG beyond k = 5 drifts from FP64 (R12): north_star's 1e-3; SD / Landweber keep 1e-4
+    assert rel_l2(xs[0][2].double().cpu().numpy()[1], xr) < (1e-3 if solver == "cg" else 1e-4)
