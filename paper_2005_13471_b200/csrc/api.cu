@@ -910,7 +910,20 @@ bsct_status reconstruct_pipe(bsct_plan p, const void *sino, void *x, int B, int 
   const size_t es = p->esize();
   const size_t sino_b = es * (size_t)p->n_angles * p->M, img_b = es * (size_t)p->N * p->N;
   const int cb = pipe_chunk(B, sino_host != nullptr);
-  const int nch = (B + cb - 1) / cb;
+  // chunk boundaries: with host buffers the first and last chunks are a quarter chunk, so that
+  // the copy before the first kernel and after the last one (the unhidden part) are short
+  std::vector<int> c0s;
+  {
+    const int edge = (sino_host && cb < B) ? std::max(1, cb / 4) : cb;
+    int c0 = 0;
+    while (c0 < B) {
+      c0s.push_back(c0);
+      const int left = B - c0;
+      c0 += (c0 == 0) ? std::min(edge, left) : (left <= cb + edge ? (left > edge ? left - edge : left) : cb);
+    }
+    c0s.push_back(B);
+  }
+  const int nch = (int)c0s.size() - 1;
   bsct_status st = pipe_resources(p, nch);
   if (st != BSCT_OK) return st;
   const char *oe = getenv("BSCT_PIPE_OVERLAP");
@@ -924,13 +937,13 @@ bsct_status reconstruct_pipe(bsct_plan p, const void *sino, void *x, int B, int 
   for (cudaStream_t o : {p->aux, p->aux2, p->hi}) CU(cudaStreamWaitEvent(o, start, 0));
   if (sino_host)
     for (int c = 0; c < nch; ++c) {
-      const int c0 = c * cb, nb = std::min(cb, B - c0);
+      const int c0 = c0s[c], nb = c0s[c + 1] - c0;
       CU(cudaMemcpyAsync((char *)sino + c0 * sino_b, (const char *)sino_host + c0 * sino_b, nb * sino_b,
                          cudaMemcpyHostToDevice, p->aux));
       CU(cudaEventRecord(evH[c], p->aux));
     }
   for (int c = 0; c < nch; ++c) {
-    const int c0 = c * cb, nb = std::min(cb, B - c0);
+    const int c0 = c0s[c], nb = c0s[c + 1] - c0;
     const char *sc = (const char *)sino + c0 * sino_b;
     char *bc = bdev + c0 * img_b;
     if (sino_host) CU(cudaStreamWaitEvent(sb, evH[c], 0));
@@ -960,7 +973,7 @@ bsct_status reconstruct_pipe(bsct_plan p, const void *sino, void *x, int B, int 
   }
   if (overlap)
     for (int c = 0; c < nch; ++c) {
-      const int c0 = c * cb, nb = std::min(cb, B - c0);
+      const int c0 = c0s[c], nb = c0s[c + 1] - c0;
       const char *bc = bdev + c0 * img_b;
       CU(cudaStreamWaitEvent(ss, evB[c], 0));
       p->launches = 0;
