@@ -161,6 +161,7 @@ __global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx,
   const int tid = threadIdx.x;
   __shared__ double w[8], sig[64], bp[16], wb[4];
   __shared__ int sgn[64], nw, nbase, P, S, imin;
+  __shared__ bool rownz[BP_PMAX * BP_SMAX];
   __shared__ double H;
   if (a >= n) return;
   const double c = cs[2 * a], s = cs[2 * a + 1];
@@ -270,6 +271,23 @@ __global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx,
       }
     }
     for (int k = 0; k < 8; ++k) Ba[(size_t)item * 8 + k] = (T)coef[k];
+    bool nz = false;
+    for (int k = 0; k < 8; ++k) nz = nz || (T)coef[k] != (T)0;
+    rownz[item] = nz;
+  }
+  __syncthreads();
+  // nonzero row range per sub-interval: rows outside the kernel's support on that sub-interval
+  // are all-zero, and K4 skips them when it builds its tables (identical sums: exact zeros)
+  if (tid < BP_PMAX) {
+    int lo = BP_SMAX, hi = -1;
+    for (int i = 0; i < BP_SMAX; ++i)
+      if (rownz[tid * BP_SMAX + i]) {
+        lo = i < lo ? i : lo;
+        hi = i;
+      }
+    if (hi < 0) lo = 1, hi = 0;  // empty range
+    ang[a].ilo[tid] = (unsigned char)lo;
+    ang[a].ihi[tid] = (unsigned char)hi;
   }
 }
 
@@ -604,7 +622,8 @@ __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int 
 #pragma unroll
         for (int k = 0; k < NC; ++k) f[sl][k] = 0.f;
       const float *Bp = Bst + p * BP_SMAX * 8;
-      for (int i = 0; i < S; ++i) {
+      const int ilo = A.ilo[p], ihi = A.ihi[p];  // basis rows outside [ilo, ihi] are zero
+      for (int i = ilo; i <= ihi; ++i) {
         float bb[8];
         Vec8<float>::load(Bp + i * 8, bb);
 #pragma unroll

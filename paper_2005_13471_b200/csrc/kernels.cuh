@@ -87,6 +87,7 @@ struct BPAngle {
   double du1, du2;  // d u / d k1, d u / d k2
   double bp[BP_PMAX];  // sub-interval starts in [0,1), bp[0] = 0, unused = +huge
   int P, S, imin, pad;
+  unsigned char ilo[BP_PMAX], ihi[BP_PMAX];  // per sub-interval: first / last nonzero basis row
 };
 size_t bp_table_floats(int n);  // size of the basis table B[n][BP_PMAX][BP_SMAX][8]
 int bp_v2_max_cells(double lx, double ly, double zeta);  // 0: geometry not supported by v2
