@@ -94,9 +94,9 @@ bsct_status bsct_gram_build(const bsct_geometry *g, bsct_dtype dt, int32_t angle
  * Plan: per-geometry device state -- per-angle box-spline tables, the filter
  * spectrum of the L x L circulant embedding of `taps` (DEVICE, full filter,
  * dtype dt; read during this call only), FFT twiddles and workspaces for up to
- * max_batch slices.  Synchronises `stream` once (table upload).  The plan owns all
- * of its memory; destroy with bsct_plan_destroy.  A plan may be used from one host
- * thread at a time.
+ * max_batch slices (0 <= max_batch <= 65535, else BSCT_EINVAL).  Synchronises `stream`
+ * once (table upload).  The plan owns all of its memory; destroy with bsct_plan_destroy.
+ * A plan may be used from one host thread at a time.
  */
 bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *taps, int32_t max_batch,
                              bsct_plan *out, bsct_stream stream);

@@ -704,6 +704,8 @@ bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *
   if (st != BSCT_OK) return st;
   if (!taps) return fail(BSCT_EINVAL, "taps is NULL");
   if (max_batch < 0) return fail(BSCT_EINVAL, "max_batch < 0");
+  // slices index gridDim.y / gridDim.z of the batched kernels (<= 65535)
+  if (max_batch > 65535) return fail(BSCT_EINVAL, "max_batch = %d exceeds 65535 (shard the stack)", max_batch);
   bsct_plan p = new bsct_plan_s();
   p->N = g->N;
   p->L = fft_size(g->N);

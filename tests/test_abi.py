@@ -94,3 +94,15 @@ def test_null_plan_rejected_everywhere(lib):
     for c in calls:
         assert c() == bsct.EINVAL
         assert b"plan" in lib.bsct_last_error()
+
+
+def test_plan_create_rejects_oversized_batch(lib):
+    """max_batch > 65535 (the batched kernels' grid limit) fails with BSCT_EINVAL before any
+    device work; so does a negative one."""
+    import paper_2005_13471_b200 as bsct
+    g = dict(N=4, lambda_x=1.0, angles=np.zeros(4), lambda_y=1.0, n_det=9, zeta=0.0)
+    s, keep = bsct._geom(g)
+    out = ctypes.c_void_p()
+    for mb in (70000, -1):
+        assert lib.bsct_plan_create(ctypes.byref(s), bsct.F32, ctypes.c_void_p(1), mb, ctypes.byref(out), None) == bsct.EINVAL
+        assert b"max_batch" in lib.bsct_last_error()
