@@ -105,6 +105,19 @@ struct FftCfg {
 
 __device__ __forceinline__ int pidx(int i) { return i + (i >> 4); }
 
+// Barrier between the stages of one group's FFT.  A group of P <= 32 threads lies inside one
+// warp (32 % P == 0), so a warp barrier orders its shared-memory exchanges; larger groups need
+// the CTA barrier.  The barrier after the last stage is always CTA-wide: callers read other
+// groups' buffers (Hermitian splits).
+template <int L>
+__device__ __forceinline__ void fft_group_sync() {
+  if constexpr (FftCfg<L>::P <= 32) {
+    __syncwarp();
+  } else {
+    __syncthreads();
+  }
+}
+
 template <typename T, int L, bool INV, int S>
 __device__ __forceinline__ void fft_stage(cplx<T> *sm, const cplx<T> *__restrict__ tw, int t) {
   using Cf = FftCfg<L>;
@@ -121,7 +134,7 @@ __device__ __forceinline__ void fft_stage(cplx<T> *sm, const cplx<T> *__restrict
 #pragma unroll
       for (int r = 0; r < R; ++r) a[u * R + r] = sm[pidx(j + r * STRIDE)];
     }
-    __syncthreads();
+    fft_group_sync<L>();
 #pragma unroll
     for (int u = 0; u < NB; ++u) {
       const int j = t + u * Cf::P;
@@ -138,7 +151,8 @@ __device__ __forceinline__ void fft_stage(cplx<T> *sm, const cplx<T> *__restrict
 #pragma unroll
       for (int r = 0; r < R; ++r) sm[pidx(base + r * Ns)] = a[u * R + r];
     }
-    __syncthreads();
+    if constexpr (S + 1 < Cf::NSTAGES) fft_group_sync<L>();
+    else __syncthreads();
     fft_stage<T, L, INV, S + 1>(sm, tw, t);
   }
 }
@@ -154,7 +168,8 @@ __device__ __forceinline__ void fft_group(cplx<T> *v, cplx<T> *sm, const cplx<T>
   dft_reg<R0, INV>(v);
 #pragma unroll
   for (int r = 0; r < R0; ++r) sm[pidx(t * R0 + r)] = v[r];
-  __syncthreads();
+  if constexpr (1 < FftCfg<L>::NSTAGES) fft_group_sync<L>();
+  else __syncthreads();
   fft_stage<T, L, INV, 1>(sm, tw, t);
 }
 

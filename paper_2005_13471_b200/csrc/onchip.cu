@@ -52,6 +52,9 @@ __global__ void __launch_bounds__(OC_THREADS) onchip_kernel(int N, int iters, co
   const int RP = ((N + CS - 1) / CS + 1) & ~1;  // rows per CTA, even (row pairs)
   const int rlo = min(N, crank * RP), rhi = min(N, rlo + RP);
   const int npairs = (rhi - rlo + 1) / 2;
+  // FP32 row pairs start at even rows (rlo is even): (ra, ra + 1) are 16-byte aligned in T1 rows
+  // when N is even
+  const bool pair16 = sizeof(T) == 4 && (N % 2) == 0;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V *T1 = reinterpret_cast<V *>(smem_raw);  // [QP][N]: this CTA's columns
@@ -120,8 +123,14 @@ __global__ void __launch_bounds__(OC_THREADS) onchip_kernel(int N, int iters, co
           const V zc = sm[pidx((L - q) & (L - 1))];
           const int own = q / QP;
           V *dst = cl.map_shared_rank(T1, own) + (size_t)(q - own * QP) * N;
-          dst[ra] = V{(T)0.5 * (z.x + zc.x), (T)0.5 * (z.y - zc.y)};
-          if (ra + 1 < rhi) dst[ra + 1] = V{(T)0.5 * (z.y + zc.y), (T)0.5 * (zc.x - z.x)};
+          const V va = V{(T)0.5 * (z.x + zc.x), (T)0.5 * (z.y - zc.y)};
+          const V vb = V{(T)0.5 * (z.y + zc.y), (T)0.5 * (zc.x - z.x)};
+          if (ra + 1 < rhi && pair16) {  // one 16-byte DSMEM store for the pair (FP32)
+            *reinterpret_cast<float4 *>(dst + ra) = make_float4((float)va.x, (float)va.y, (float)vb.x, (float)vb.y);
+          } else {
+            dst[ra] = va;
+            if (ra + 1 < rhi) dst[ra + 1] = vb;
+          }
         }
       __syncthreads();  // sm is rewritten by the next round
     }
@@ -183,8 +192,14 @@ __global__ void __launch_bounds__(OC_THREADS) onchip_kernel(int N, int iters, co
         if (valid) {
           const int own = q / QP;
           const V *src = cl.map_shared_rank(T1, own) + (size_t)(q - own * QP) * N;
-          xa = src[ra];
-          if (ra + 1 < rhi) xb = src[ra + 1];
+          if (ra + 1 < rhi && pair16) {  // one 16-byte DSMEM load for the pair (FP32)
+            const float4 f = *reinterpret_cast<const float4 *>(src + ra);
+            xa = V{(T)f.x, (T)f.y};
+            xb = V{(T)f.z, (T)f.w};
+          } else {
+            xa = src[ra];
+            if (ra + 1 < rhi) xb = src[ra + 1];
+          }
         }
         if (q == 0 || q == L / 2) { xa.y = 0; xb.y = 0; }  // real rows: DC and Nyquist are real
         sm[pidx(q)] = V{xa.x - xb.y, xa.y + xb.x};
@@ -299,11 +314,11 @@ static cudaError_t onchip_L(int N, int B, int iters, int mode, const T *b, T *x,
 }
 
 // Opt-in (BSCT_ONCHIP=1): measured on B200 (tools/time_onchip.py) this version is slower than the
-// fused 3-launch iteration -- config 2 (N = 256, 50 CG iterations): 5.1 ms vs 1.4 ms for one slice,
-// 22 ms vs 11 ms for 128 slices; config 1 (N = 64, FP64): 0.57 vs 0.42 ms.  Its block-level
-// radix-16 FFT groups with CTA barriers, 8-byte DSMEM scatters and three cluster barriers per
-// iteration cost ~100 us per iteration on 8 SMs, while the fused passes spread even one slice
-// over many SMs.  Kept as the parity-tested cluster/DSMEM design (NEXT-2, first version).
+// fused 3-launch iteration -- config 2 (N = 256, 50 CG iterations): 4.4 ms vs 1.6 ms for 16 slices,
+// 17.9 ms vs 11.0 ms for 128 slices (16-byte DSMEM row-pair accesses; 22 ms with 8-byte ones);
+// config 1 (N = 64, FP64): 0.57 vs 0.36 ms.  The block-level FFT groups, the DSMEM scatter/gather
+// and three cluster barriers per iteration cost more than the HBM traffic they save at these
+// sizes.  Kept as the parity-tested cluster/DSMEM design (NEXT-2, first version).
 bool onchip_enabled() {
   const char *e = getenv("BSCT_ONCHIP");
   return e && e[0] == '1';
