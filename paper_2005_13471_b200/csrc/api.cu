@@ -303,7 +303,8 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMalloc(&p->p, sizeof(T) * nn * Bz));
   CU(cudaMalloc(&p->q, sizeof(T) * nn * Bz));
   CU(cudaMalloc((void **)&p->alpha, sizeof(double) * Bz));
-  CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * pass_b_blocks(L, p->dt == BSCT_F32)));
+  // gamma partials: room for either pass-B layout (BSCT_PASSB_V1 is read per call)
+  CU(cudaMalloc((void **)&p->gpart, sizeof(double) * Bz * std::max(pass_b_blocks(L, false), pass_b_blocks(L, true))));
   // <r,r> partials: room for either pass layout (the warp passes use more CTAs per slice)
   const size_t nrp = std::max((size_t)vec_blocks(N), (size_t)2 * (fused_parts(N, L, false) + fused_parts(N, L, true)));
   CU(cudaMalloc((void **)&p->rpart, sizeof(double) * Bz * nrp));

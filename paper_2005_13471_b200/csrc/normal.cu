@@ -200,6 +200,112 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
   }
 }
 
+// ---------------------------------------------------------------- pass B, L = 512 (FP32)
+// Half-warp 16 x 32 four-step FFT per column (two columns per warp): lane t < 16 holds
+// x[t + 16 r] (r < 32; rows >= N <= 256 are zero, so r < 16), DFT_32 over r in registers,
+// twiddle W_512^{t j} (= W_1024^{2 t j}, the L = 1024 table), a padded 32 x 17 transpose so that
+// lane t holds columns j = t and t + 16, two in-register DFT_16 over t: X[j + 32 k].  The inverse
+// runs the steps backwards and forms only the first N <= 256 outputs.
+#ifndef BSCT_PB5_WARPS
+#define BSCT_PB5_WARPS 4
+#endif
+#ifndef BSCT_PB5_MINB
+#define BSCT_PB5_MINB 4
+#endif
+constexpr int PB5_WARPS = BSCT_PB5_WARPS;
+
+template <bool FULL>
+__global__ void __launch_bounds__(PB5_WARPS * 32, BSCT_PB5_MINB) pass_b_512_kernel(int N, float2 *__restrict__ T1,
+                                                                     const float *__restrict__ S,
+                                                                     const float2 *__restrict__ tw1024,
+                                                                     double *__restrict__ gpart) {
+  constexpr int L = 512, Q = L / 2 + 1;
+  __shared__ float2 twl[32 * 32];
+  __shared__ float2 trs[PB5_WARPS][2][32 * 17];
+  __shared__ double red[PB5_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, h = lane >> 4, t = lane & 15;
+  // twl holds W_1024^{r c} (symmetric in r, c) with each row's even columns first: entry (r, c)
+  // at r * 32 + (c >> 1) + 16 * (c & 1), so that both W_512^{t j} = (j, 2t) over lanes t (forward)
+  // and W_512^{j tt} = (2 tt, j) over lanes j = t or t + 16 (inverse) hit 16 distinct bank pairs
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {
+    const int r = i >> 5, c = i & 31;
+    twl[r * 32 + (c >> 1) + 16 * (c & 1)] = tw1024[i];
+  }
+  __syncthreads();
+  const int b = blockIdx.y;
+  const int q0 = (blockIdx.x * PB5_WARPS + warp) * 2 + h;
+  const bool live = q0 < Q;  // the last half-warps recompute column Q - 1 and store nothing
+  const int q = live ? q0 : Q - 1;
+  float2 *col = T1 + ((size_t)b * Q + q) * N;
+  float2 *tr = trs[warp][h];
+  float2 v[32];
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int n = t + 16 * r;
+    v[r] = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
+  }
+  dft32<false, true>(v);  // v[j] = sum_r x[t + 16 r] W_32^{r j}
+#pragma unroll
+  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twl[j * 32 + t]);  // W_512^{t j} = entry (j, 2t)
+#pragma unroll
+  for (int j = 0; j < 32; ++j) tr[j * 17 + t] = v[j];
+  __syncwarp();
+  float2 a0[16], a1[16];
+#pragma unroll
+  for (int tt = 0; tt < 16; ++tt) {
+    a0[tt] = tr[t * 17 + tt];
+    a1[tt] = tr[(t + 16) * 17 + tt];
+  }
+  __syncwarp();
+  dft_reg<16, false>(a0);  // a0[k] = X[t + 32 k]
+  dft_reg<16, false>(a1);  // a1[k] = X[t + 16 + 32 k]
+  const float *Sq = S + (size_t)q * L;
+  float g2[2] = {0.f, 0.f};
+#pragma unroll
+  for (int k = 0; k < 16; ++k) {
+    const float s0 = Sq[t + 32 * k], s1 = Sq[t + 16 + 32 * k];
+    g2[0] = fmaf(s0, fmaf(a0[k].x, a0[k].x, a0[k].y * a0[k].y), g2[0]);
+    g2[1] = fmaf(s1, fmaf(a1[k].x, a1[k].x, a1[k].y * a1[k].y), g2[1]);
+    a0[k] = float2{a0[k].x * s0, a0[k].y * s0};
+    a1[k] = float2{a1[k].x * s1, a1[k].y * s1};
+  }
+  double gam = (double)g2[0] + (double)g2[1];
+  if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
+  if (!live) gam = 0.0;
+  dft_reg<16, true>(a0);  // a0[tt] = U[j = t][tt]
+  dft_reg<16, true>(a1);  // a1[tt] = U[j = t + 16][tt]
+#pragma unroll
+  for (int tt = 1; tt < 16; ++tt) {
+    a0[tt] = cmulc(a0[tt], twl[tt * 64 + (t >> 1) + 16 * (t & 1)]);       // entry (2 tt, t)
+    a1[tt] = cmulc(a1[tt], twl[tt * 64 + 8 + (t >> 1) + 16 * (t & 1)]);   // entry (2 tt, t + 16)
+  }
+#pragma unroll
+  for (int tt = 0; tt < 16; ++tt) {
+    tr[t * 17 + tt] = a0[tt];
+    tr[(t + 16) * 17 + tt] = a1[tt];
+  }
+  __syncwarp();
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = tr[j * 17 + t];  // lane t: U[j][t]
+  __syncwarp();
+  dft32<true>(v);  // v[r] = z[t + 16 r]
+#pragma unroll
+  for (int r = 0; r < 16; ++r) {
+    const int n = t + 16 * r;
+    if (live && (FULL || n < N)) col[n] = v[r];
+  }
+  if (gpart) {  // deterministic CTA reduction
+    for (int o = 16; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o);
+    if (lane == 0) red[warp] = gam;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double tot = 0;
+      for (int i = 0; i < PB5_WARPS; ++i) tot += red[i];
+      gpart[(size_t)b * gridDim.x + blockIdx.x] = tot;
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pass C
 template <typename T, int L>
 __global__ void __launch_bounds__(FftLaunch<L>::THREADS) pass_c_kernel(int N, const cplx<T> *__restrict__ T1,
@@ -395,6 +501,18 @@ static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T>
       return cudaGetLastError();
     }
   }
+  if constexpr (std::is_same<T, float>::value && L == 512) {
+    const float2 *twl = tw1024_table();
+    if (!twl) return cudaErrorMemoryAllocation;
+    if (pass_b_warp_enabled()) {
+      const dim3 grid((L / 2 + 1 + 2 * PB5_WARPS - 1) / (2 * PB5_WARPS), B);
+      if (N == L / 2)
+        pass_b_512_kernel<true><<<grid, PB5_WARPS * 32, 0, s>>>(N, T1, S, twl, gpart);
+      else
+        pass_b_512_kernel<false><<<grid, PB5_WARPS * 32, 0, s>>>(N, T1, S, twl, gpart);
+      return cudaGetLastError();
+    }
+  }
   constexpr int G = FftLaunchB<L>::G;
   const size_t sm = (size_t)G * FftCfg<L>::SMEM * sizeof(cplx<T>);
   cudaError_t e = set_smem(pass_b_kernel<T, L>, sm);
@@ -433,6 +551,7 @@ bool pass_b_warp_enabled() {
 
 int pass_b_blocks(int L, bool fp32) {
   if (fp32 && L == 1024 && pass_b_warp_enabled()) return (1024 / 2 + 1 + PB_WARPS - 1) / PB_WARPS;  // FP32 warp kernel
+  if (fp32 && L == 512 && pass_b_warp_enabled()) return (512 / 2 + 1 + 2 * PB5_WARPS - 1) / (2 * PB5_WARPS);
   switch (L) {
     case 2: return (2 / 2 + 1 + FftLaunchB<2>::G - 1) / FftLaunchB<2>::G;
     case 4: return (4 / 2 + 1 + FftLaunchB<4>::G - 1) / FftLaunchB<4>::G;
