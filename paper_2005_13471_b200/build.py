@@ -27,6 +27,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", f"-I{INCLUDE}", f"-I{CSRC}"]
+FLAGS += os.environ.get("BSCT_NVCC_EXTRA", "").split()  # e.g. -DBSCT_NO_F32X2 for A/B variants
 
 
 def _sources():

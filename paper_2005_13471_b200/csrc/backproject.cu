@@ -629,8 +629,17 @@ __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int 
 #pragma unroll
         for (int sl = 0; sl < SB; ++sl) {
           const float gv = gst[sl * gseg + cc + i];
+          if constexpr (NC % 2 == 0) {  // coefficient pairs on the packed FP32x2 pipe
 #pragma unroll
-          for (int k = 0; k < NC; ++k) f[sl][k] = fmaf(gv, bb[k], f[sl][k]);
+            for (int k = 0; k < NC; k += 2) {
+              const float2 r = cfma2(float2{gv, gv}, float2{bb[k], bb[k + 1]}, float2{f[sl][k], f[sl][k + 1]});
+              f[sl][k] = r.x;
+              f[sl][k + 1] = r.y;
+            }
+          } else {
+#pragma unroll
+            for (int k = 0; k < NC; ++k) f[sl][k] = fmaf(gv, bb[k], f[sl][k]);
+          }
         }
       }
       float *dst = tab + cc * P + p;
@@ -668,12 +677,25 @@ __global__ void __launch_bounds__(BP_THREADS, 2) bp_v3_kernel(int N, int B, int 
       }
       const float tau = phm - bsel;
       const float *e = tb + ci * P + po;
+      if constexpr (SB % 2 == 0) {  // slice pairs on the packed FP32x2 pipe (same tau)
 #pragma unroll
-      for (int sl = 0; sl < SB; ++sl) {
-        float rr = e[(sl * NC + NC - 1) * PL];
+        for (int sl = 0; sl < SB; sl += 2) {
+          float2 rr{e[(sl * NC + NC - 1) * PL], e[((sl + 1) * NC + NC - 1) * PL]};
 #pragma unroll
-        for (int k = NC - 2; k >= 0; --k) rr = fmaf(rr, tau, e[(sl * NC + k) * PL]);
-        acc[sl][j] += rr;
+          for (int k = NC - 2; k >= 0; --k)
+            rr = cfma2(rr, float2{tau, tau}, float2{e[(sl * NC + k) * PL], e[((sl + 1) * NC + k) * PL]});
+          const float2 sum = cadd(float2{acc[sl][j], acc[sl + 1][j]}, rr);
+          acc[sl][j] = sum.x;
+          acc[sl + 1][j] = sum.y;
+        }
+      } else {
+#pragma unroll
+        for (int sl = 0; sl < SB; ++sl) {
+          float rr = e[(sl * NC + NC - 1) * PL];
+#pragma unroll
+          for (int k = NC - 2; k >= 0; --k) rr = fmaf(rr, tau, e[(sl * NC + k) * PL]);
+          acc[sl][j] += rr;
+        }
       }
     }
   }

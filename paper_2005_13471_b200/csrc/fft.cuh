@@ -48,7 +48,8 @@ __device__ __forceinline__ V twiddle16(V v, int m) {
   if (m == 4) return INV ? V{-v.y, v.x} : V{v.y, -v.x};
   const S c = (S)cos16(m);
   const S s = INV ? (S)sin16(m) : -(S)sin16(m);
-  return V{v.x * c - v.y * s, v.x * s + v.y * c};
+  if constexpr (sizeof(S) == 4) return crot(v, c, s);
+  else return V{v.x * c - v.y * s, v.x * s + v.y * c};
 }
 
 __host__ __device__ constexpr int bitrev(int x, int bits) {

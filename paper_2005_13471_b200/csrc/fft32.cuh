@@ -48,7 +48,7 @@ __device__ __forceinline__ float2 twiddle32(float2 v, int m) {
   if (m == 24) return INV ? float2{v.y, -v.x} : float2{-v.y, v.x};
   const float c = (float)cos32(m);
   const float s = INV ? (float)sin32(m) : -(float)sin32(m);
-  return float2{v.x * c - v.y * s, v.x * s + v.y * c};
+  return crot(v, c, s);
 }
 
 __host__ __device__ constexpr int bitrev5(int x) {

@@ -167,14 +167,15 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
     const float *Sq = S + (size_t)q * L + lane;
     // per-lane Parseval partials in FP32 (4 interleaved sums of 8 positive terms each:
     // relative error <= 8 eps), combined in FP64 across lanes and CTAs
-    float g4[4] = {0.f, 0.f, 0.f, 0.f};
+    // (packed: g2[k & 1] += (s x, s y) * (x, y), then v = s v)
+    float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};
 #pragma unroll
     for (int k = 0; k < 32; ++k) {
-      const float sv = Sq[32 * k];
-      g4[k & 3] = fmaf(sv, fmaf(v[k].x, v[k].x, v[k].y * v[k].y), g4[k & 3]);
-      v[k] = float2{v[k].x * sv, v[k].y * sv};
+      const float2 w = cscale(v[k], Sq[32 * k]);
+      g2[k & 1] = cfma2(w, v[k], g2[k & 1]);
+      v[k] = w;
     }
-    gam = (double)(g4[0] + g4[1]) + (double)(g4[2] + g4[3]);
+    gam = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
     if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
     if (!live) gam = 0.0;
     dft32<true>(v);  // over k: v[a] = U[lane][a]
@@ -260,16 +261,16 @@ __global__ void __launch_bounds__(PB5_WARPS * 32, BSCT_PB5_MINB) pass_b_512_kern
   dft_reg<16, false>(a0);  // a0[k] = X[t + 32 k]
   dft_reg<16, false>(a1);  // a1[k] = X[t + 16 + 32 k]
   const float *Sq = S + (size_t)q * L;
-  float g2[2] = {0.f, 0.f};
+  float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};  // packed Parseval partials, as in pass_b_1024_kernel
 #pragma unroll
   for (int k = 0; k < 16; ++k) {
-    const float s0 = Sq[t + 32 * k], s1 = Sq[t + 16 + 32 * k];
-    g2[0] = fmaf(s0, fmaf(a0[k].x, a0[k].x, a0[k].y * a0[k].y), g2[0]);
-    g2[1] = fmaf(s1, fmaf(a1[k].x, a1[k].x, a1[k].y * a1[k].y), g2[1]);
-    a0[k] = float2{a0[k].x * s0, a0[k].y * s0};
-    a1[k] = float2{a1[k].x * s1, a1[k].y * s1};
+    const float2 w0 = cscale(a0[k], Sq[t + 32 * k]), w1 = cscale(a1[k], Sq[t + 16 + 32 * k]);
+    g2[0] = cfma2(w0, a0[k], g2[0]);
+    g2[1] = cfma2(w1, a1[k], g2[1]);
+    a0[k] = w0;
+    a1[k] = w1;
   }
-  double gam = (double)g2[0] + (double)g2[1];
+  double gam = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
   if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
   if (!live) gam = 0.0;
   dft_reg<16, true>(a0);  // a0[tt] = U[j = t][tt]
