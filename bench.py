@@ -378,7 +378,7 @@ def run_ours(args):
                 "algorithmic_bytes": B * 4 * (n_ang * (M + 50) + N * N),
                 "peak_source": peak_src,
                 "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6); "
-                        "K4 v3 evaluates it from per-tile tables and is shared-memory bound (ncu L1/smem 81%)"}
+                        "K4 v3 evaluates it from per-tile tables and is shared-memory bound (ncu L1/smem 84%)"}
     else:
         # HBM-bound FFT passes: compulsory bytes of the pass per launch (K5)
         byts = cg_bytes.get(dom, 0)

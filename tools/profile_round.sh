@@ -11,5 +11,8 @@ ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/la
 echo "launch rc=$?"
 CMD2="python bench.py --slices 64 --iters 2 --steps 1 --warmup 1 --no-e2e --no-cpu"
 $CMD2 > $O/plain_full.log 2>&1 && \
-ncu --set full --clock-control none --import-source on -k regex:"bp_v3|pass_[abc]_1024|correction|gram_taps" -s 4 -c 7 -o $O/prof_full $CMD2 > $O/ncu_full.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"pass_[abc]_1024|correction|gram_taps" -s 4 -c 7 -o $O/prof_full $CMD2 > $O/ncu_full.log 2>&1
 echo "full rc=$?"
+# K4 separately (its first launches would be skipped above)
+ncu --set full --clock-control none --import-source on -k regex:bp_v3 -s 1 -c 1 -o $O/prof_bp $CMD2 > $O/ncu_bp.log 2>&1
+echo "bp rc=$?"
