@@ -562,6 +562,153 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_c_1024_kernel(in
   if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
 }
 
+// ---------------------------------------------------------------- pass C, L = 512 (FP32 half-warp FFTs)
+// Same contract as cg_pass_c_kernel<float, 512> (32 rows per CTA = the generic pass A's
+// partition, so the rpart layout is shared).  T1 staged as in cg_pass_c_1024_kernel ([q][17]
+// row-pair float4 slots); each half-warp inverts one row pair with the 16 x 32 four-step FFT of
+// pass_b_512_kernel run backwards: lane t takes Z[t + 32 k] and Z[t + 16 + 32 k] (k < 16),
+// two inverse DFT_16, conj W_512 twiddles (even-columns-first table), a padded 32 x 17
+// transpose, and one inverse DFT_32 forming only z[t + 16 r], r < 16 (N <= 256).
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) cg_pass_c_512_kernel(int N, int k, int gparts, const float2 *__restrict__ T1,
+                                                               float *__restrict__ x, float *__restrict__ r,
+                                                               const float2 *__restrict__ tw1024, FusedWork w) {
+  constexpr int L = 512, Q = L / 2 + 1, ROWS = 32, NP = ROWS / 2, RS = NP + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] row pairs, later [NP][32][17] float2
+  __shared__ float2 twl[32 * 32];
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = lane & 15;
+  const int pair = 2 * warp + (lane >> 4);
+  const int b = blockIdx.y;
+  const int row0 = blockIdx.x * ROWS;
+  const int rows = min(ROWS, N - row0);
+  const float2 *T1s = T1 + (size_t)b * Q * N + row0;
+  for (int i = threadIdx.x; i < Q * NP; i += blockDim.x) {
+    const int q = i / NP, pr = i % NP, rp = 2 * pr;
+    float4 *dst = st + q * RS + pr;
+    const float2 *src = T1s + (size_t)q * N + rp;
+    if (rp + 1 < rows) {
+      if (!(N & 1)) {
+        cp_async16_g(dst, src);
+      } else {
+        cp_async8_g(dst, src);
+        cp_async8_g(reinterpret_cast<float2 *>(dst) + 1, src + 1);
+      }
+    } else if (rp < rows) {
+      cp_async8_g(dst, src);
+      reinterpret_cast<float2 *>(dst)[1] = float2{0.f, 0.f};
+    } else {
+      *dst = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {  // layout of pass_b_512_kernel
+    const int rr = i >> 5, c = i & 31;
+    twl[rr * 32 + (c >> 1) + 16 * (c & 1)] = tw1024[i];
+  }
+  double rho = 0.0;
+  if (MODE == 3) {
+  } else if (MODE == 0) {
+    rho = w.rho[(size_t)b * w.rho_stride + k];
+  } else {
+    rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+  }
+  double alpha = 0.0;
+  if (MODE == 3) {
+  } else if (MODE == 2) {
+    alpha = *w.tau;
+  } else {
+    const double gam = cta_reduce_parts(w.gpart + (size_t)b * gparts, gparts, red);
+    const bool bad = rho > 0 && !(gam > 0);
+    const bool frozen = bad || (w.flags && w.flags[b]);
+    alpha = (rho > 0 && !frozen) ? rho / gam : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
+  }
+  if (MODE != 3 && blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
+  const float al = (float)alpha;
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // Z[q] = X_a[q] + i X_b[q] (q <= 256), Z[L - q] = conj X_a[q] + i conj X_b[q]
+  auto zdir = [&](int q) {
+    float4 e = st[q * RS + pair];
+    if (q == 0 || q == L / 2) { e.y = 0.f; e.w = 0.f; }  // DC / Nyquist of real rows
+    return float2{e.x - e.w, e.y + e.z};
+  };
+  auto zmir = [&](int q) {
+    const float4 e = st[(L - q) * RS + pair];
+    return float2{e.x + e.w, e.z - e.y};
+  };
+  float2 a0[16], a1[16];
+#pragma unroll
+  for (int kk = 0; kk < 16; ++kk) {
+    const int q0 = t + 32 * kk, q1 = q0 + 16;
+    a0[kk] = (kk < 8 || (kk == 8 && t == 0)) ? zdir(q0) : zmir(q0);
+    a1[kk] = kk < 8 ? zdir(q1) : zmir(q1);
+  }
+  // this half-warp's r (x) rows into registers: latency overlaps the FFT below
+  const int ra = row0 + 2 * pair;
+  const bool ha = ra < N, hb = ra + 1 < N;
+  float *r0 = r + ((size_t)b * N + ra) * N, *x0 = x + ((size_t)b * N + ra) * N;
+  float rv[2][16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int n = t + 16 * m;
+    rv[0][m] = (MODE != 3 && ha && n < N) ? r0[n] : 0.f;
+    rv[1][m] = (MODE != 3 && hb && n < N) ? r0[N + n] : 0.f;
+  }
+  dft_reg<16, true>(a0);  // over k: a0[tt] = U[j = t][tt]
+  dft_reg<16, true>(a1);  // a1[tt] = U[j = t + 16][tt]
+#pragma unroll
+  for (int tt = 1; tt < 16; ++tt) {
+    a0[tt] = cmulc(a0[tt], twl[tt * 64 + (t >> 1) + 16 * (t & 1)]);      // W_512^{t tt}
+    a1[tt] = cmulc(a1[tt], twl[tt * 64 + 8 + (t >> 1) + 16 * (t & 1)]);  // W_512^{(t + 16) tt}
+  }
+  __syncthreads();  // staging area becomes the transpose buffers
+  float2 *tr = reinterpret_cast<float2 *>(smem_raw) + pair * (32 * 17);
+#pragma unroll
+  for (int tt = 0; tt < 16; ++tt) {
+    tr[t * 17 + tt] = a0[tt];
+    tr[(t + 16) * 17 + tt] = a1[tt];
+  }
+  __syncwarp();
+  float2 v[32];
+#pragma unroll
+  for (int j = 0; j < 32; ++j) v[j] = tr[j * 17 + t];  // lane t: U[j][t]
+  dft32<true>(v);                                       // v[m] = z[t + 16 m] = y_a + i y_b
+  float ac = 0.f;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const int n = t + 16 * m;
+    if (n < N) {
+      if (MODE == 3) {  // y = G x into the r pointer
+        if (ha) r0[n] = v[m].x;
+        if (hb) r0[N + n] = v[m].y;
+        continue;
+      }
+      if (ha) {
+        if (MODE != 0) x0[n] = fmaf(al, rv[0][m], x0[n]);
+        const float tv = fmaf(-al, v[m].x, rv[0][m]);
+        r0[n] = tv;
+        ac = fmaf(tv, tv, ac);
+      }
+      if (hb) {
+        if (MODE != 0) x0[N + n] = fmaf(al, rv[1][m], x0[N + n]);
+        const float tv = fmaf(-al, v[m].y, rv[1][m]);
+        r0[N + n] = tv;
+        ac = fmaf(tv, tv, ac);
+      }
+    }
+  }
+  if (MODE == 3) return;
+  const double s = cta_sum((double)ac, red);
+  if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
+}
+
 // ---------------------------------------------------------------- final: rho_K, resid, CG x update
 template <typename T>
 __global__ void __launch_bounds__(256) cg_final_kernel(long n, int K, int cg, T *__restrict__ x,
@@ -698,6 +845,18 @@ static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *
       if (e != cudaSuccess) return e;
       cg_pass_c_1024_kernel<MODE, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, gparts, T1, x, r, twl, w,
                                                                                    bulk_stage_enabled());
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (std::is_same<T, float>::value && L == 512) {
+    static_assert(2 * FftLaunch<512>::G == 32, "cg_pass_c_512_kernel covers the generic pass A's 32-row partition");
+    if (pass_c_warp_enabled()) {
+      const float2 *twl = tw1024_table();
+      if (!twl) return cudaErrorMemoryAllocation;
+      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 17;
+      cudaError_t e = cg_set_smem(cg_pass_c_512_kernel<MODE>, sm);
+      if (e != cudaSuccess) return e;
+      cg_pass_c_512_kernel<MODE><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, gparts, T1, x, r, twl, w);
       return cudaGetLastError();
     }
   }

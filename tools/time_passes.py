@@ -36,5 +36,9 @@ for name, env in (("warp", {}), ("generic B", {"BSCT_PASSB_V1": "1"}),
         torch.cuda.synchronize()
         ts.append(e0.elapsed_time(e1))
     ms = min(ts)
+    plan.profile(True)
+    bsct.cg_solve(plan, b, x, K, "cg")
+    prof = {k: round(v[0], 2) for k, v in plan.profile_read().items() if v[0] > 0.05}
+    plan.profile(False)
     print(f"config {ci} N={N} L={plan.L} B={B} K={K} {name:12s}: {ms:8.2f} ms  "
-          f"{B * K / ms * 1e3:10.0f} slice-iter/s  {ms / K * 1e3 / B:7.2f} us/slice-iter", flush=True)
+          f"{B * K / ms * 1e3:10.0f} slice-iter/s  {ms / K * 1e3 / B:7.2f} us/slice-iter  {prof}", flush=True)
