@@ -305,6 +305,155 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(in
   }
 }
 
+// ---------------------------------------------------------------- pass A (CG), L = 512 (FP32 half-warp FFTs)
+// Same contract as cg_pass_a_kernel<float, 512> (32 rows per CTA).  Streaming phase as in
+// cg_pass_a_1024_kernel (p rows kept in shared memory, row stride 264 floats so that the two
+// half-warps of a warp read different banks); each half-warp transforms one row pair
+// (z = p_a + i p_b) with the 16 x 32 four-step FFT of pass_b_512_kernel, which leaves
+// Z[t + 32 k] and Z[t + 16 + 32 k] in lane t; Z[L - q] sits in lane 16 - t, registers 15 - k
+// of the other set (lane 0: its own registers), fetched with one shuffle per register.
+template <int VW>
+__global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, float *__restrict__ x,
+                                                               const float *__restrict__ r, float *__restrict__ p,
+                                                               float2 *__restrict__ T1,
+                                                               const float2 *__restrict__ tw1024, FusedWork w) {
+  constexpr int L = 512, Q = L / 2 + 1, ROWS = 32, NP = ROWS / 2, RS = NP + 1, PW = 256, PWS = 264, NT = 256;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *ps = reinterpret_cast<float *>(smem_raw);    // [ROWS][PWS] new p rows
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [Q][RS] output staging (after the FFTs)
+  float2 *trb = reinterpret_cast<float2 *>(smem_raw); // [NP][32][17] transposes
+  __shared__ float2 twl[32 * 32];
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, t = lane & 15, h = lane >> 4;
+  const int pair = 2 * warp + h;
+  const int b = blockIdx.y;
+  for (int i = threadIdx.x; i < 32 * 32; i += blockDim.x) {  // layout of pass_b_512_kernel
+    const int rr = i >> 5, c = i & 31;
+    twl[rr * 32 + (c >> 1) + 16 * (c & 1)] = tw1024[i];
+  }
+  float be = 0.f, al = 0.f;
+  auto scalars = [&]() {
+    const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    double beta = 0.0, alpha_prev = 0.0;
+    if (k > 0) {
+      const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
+      beta = rho_prev > 0 ? rho / rho_prev : 0.0;
+      alpha_prev = w.alpha[b];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+    be = (float)beta;
+    al = (float)alpha_prev;
+  };
+  const int row0 = blockIdx.x * ROWS;
+  const int rows = min(ROWS, N - row0);
+  const size_t so = (size_t)b * N * N + (size_t)row0 * N;
+  constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
+  static_assert(ITEMS % (UB * NT) == 0, "every thread runs the same number of batches (the first one reduces)");
+  for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
+    float pv[UB][VW], rv[UB][VW], xv[UB][VW];
+    bool ok[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int i = i0 + u * NT;
+      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+      ok[u] = rr < rows && j < N;
+      if (ok[u]) {
+        const size_t e = so + (size_t)rr * N + j;
+        vload<float, VW>(pv[u], p + e);
+        vload<float, VW>(rv[u], r + e);
+        vload<float, VW>(xv[u], x + e);
+      }
+    }
+    if (i0 == (int)threadIdx.x) scalars();  // first batch: uniform across the CTA
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int i = i0 + u * NT;
+      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+      if (ok[u]) {
+        const size_t e = so + (size_t)rr * N + j;
+#pragma unroll
+        for (int c = 0; c < VW; ++c) {
+          xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
+          pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+        }
+        vstore<float, VW>(x + e, xv[u]);
+        vstore<float, VW>(p + e, pv[u]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
+      }
+      vstore<float, VW>(ps + rr * PWS + j, pv[u]);
+    }
+  }
+  __syncthreads();
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = float2{ps[(2 * pair) * PWS + t + 16 * m], ps[(2 * pair + 1) * PWS + t + 16 * m]};
+  __syncthreads();  // ps becomes the transpose buffers
+  dft32<false, true>(v);  // over m (v[16..31] = 0): v[j] = sum_m z[t + 16 m] W_32^{m j}
+#pragma unroll
+  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twl[j * 32 + t]);  // W_512^{t j}
+  float2 *tr = trb + pair * (32 * 17);
+#pragma unroll
+  for (int j = 0; j < 32; ++j) tr[j * 17 + t] = v[j];
+  __syncwarp();
+  float2 a0[16], a1[16];
+#pragma unroll
+  for (int tt = 0; tt < 16; ++tt) {
+    a0[tt] = tr[t * 17 + tt];
+    a1[tt] = tr[(t + 16) * 17 + tt];
+  }
+  dft_reg<16, false>(a0);  // a0[kk] = Z[t + 32 kk]
+  dft_reg<16, false>(a1);  // a1[kk] = Z[t + 16 + 32 kk]
+  __syncthreads();  // transposes done CTA-wide: the area becomes the output staging tile
+  const int src = (h << 4) | ((16 - t) & 15);
+#pragma unroll
+  for (int kk = 0; kk <= 8; ++kk) {
+    // partner of Z[t + 32 kk] is Z[L - q] = a1[15 - kk] of lane 16 - t (lane 0: its own a0[16 - kk])
+    float2 zc0, zc1;
+    const float2 s0 = a1[(15 - kk) & 15], s1 = a0[(15 - kk) & 15];
+    zc0.x = __shfl_sync(0xffffffffu, s0.x, src);
+    zc0.y = __shfl_sync(0xffffffffu, s0.y, src);
+    zc1.x = __shfl_sync(0xffffffffu, s1.x, src);
+    zc1.y = __shfl_sync(0xffffffffu, s1.y, src);
+    if (t == 0) {
+      zc0 = a0[(16 - kk) & 15];
+      zc1 = a1[(15 - kk) & 15];
+    }
+    if (kk < 8 || t == 0) {
+      const float2 z = a0[kk & 15];
+      const int q = t + 32 * kk;
+      st[q * RS + pair] = make_float4(0.5f * (z.x + zc0.x), 0.5f * (z.y - zc0.y), 0.5f * (z.y + zc0.y), 0.5f * (zc0.x - z.x));
+    }
+    if (kk < 8) {
+      const float2 z = a1[kk];
+      const int q = t + 16 + 32 * kk;
+      st[q * RS + pair] = make_float4(0.5f * (z.x + zc1.x), 0.5f * (z.y - zc1.y), 0.5f * (z.y + zc1.y), 0.5f * (zc1.x - z.x));
+    }
+  }
+  __syncthreads();
+  float2 *T1s = T1 + (size_t)b * Q * N + row0;
+  for (int i = threadIdx.x; i < Q * NP; i += blockDim.x) {
+    const int q = i / NP, pr = i % NP, rp = 2 * pr;
+    if (rp >= rows) continue;
+    const float4 e = st[q * RS + pr];
+    float2 *dst = T1s + (size_t)q * N + rp;
+    if (rp + 1 < rows) {
+      if (!(N & 1)) {
+        *reinterpret_cast<float4 *>(dst) = e;
+      } else {
+        dst[0] = float2{e.x, e.y};
+        dst[1] = float2{e.z, e.w};
+      }
+    } else {
+      dst[0] = float2{e.x, e.y};
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pass C: inverse row DFTs fused with the r update
 // MODE 0: CG (x deferred to pass A); 1: steepest descent; 2: Landweber (alpha = tau)
 template <typename T, int L, int MODE, int VW>
@@ -815,6 +964,24 @@ static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx
         cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, false, WROWS>, sm);
         if (e != cudaSuccess) return e;
         cg_pass_a_1024_kernel<1, false, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, x, r, p, T1, twl, w);
+      }
+      return cudaGetLastError();
+    }
+  }
+  if constexpr (std::is_same<T, float>::value && L == 512) {
+    if (pass_c_warp_enabled()) {
+      const float2 *twl = tw1024_table();
+      if (!twl) return cudaErrorMemoryAllocation;
+      constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 17;
+      static_assert(sm >= sizeof(float) * 32 * 264 && sm >= sizeof(float2) * 16 * 32 * 17, "pass A 512 smem");
+      if (can_vec<T>(N, x, r, p)) {
+        cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<4>, sm);
+        if (e != cudaSuccess) return e;
+        cg_pass_a_512_kernel<4><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+      } else {
+        cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<1>, sm);
+        if (e != cudaSuccess) return e;
+        cg_pass_a_512_kernel<1><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
       }
       return cudaGetLastError();
     }
