@@ -333,7 +333,7 @@ template <typename T>
 bsct_status normal_apply_t(bsct_plan p, const T *x, T *y, int B, double *gpart, cudaStream_t s) {
   auto *T1 = (cplx<T> *)p->T1;
   auto *tw = (const cplx<T> *)p->tw;
-  const bool warp = std::is_same<T, float>::value && p->L == 1024 && pass_c_warp_enabled();
+  const bool warp = std::is_same<T, float>::value && (p->L == 1024 || p->L == 512) && pass_c_warp_enabled();
   if (warp)
     LAUNCH(p, BSCT_K_PASS_A, 1, (warp_apply_a(p->N, p->L, B, (const float *)x, (float2 *)T1, s)));
   else

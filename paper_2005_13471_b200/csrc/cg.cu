@@ -312,7 +312,7 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(in
 // (z = p_a + i p_b) with the 16 x 32 four-step FFT of pass_b_512_kernel, which leaves
 // Z[t + 32 k] and Z[t + 16 + 32 k] in lane t; Z[L - q] sits in lane 16 - t, registers 15 - k
 // of the other set (lane 0: its own registers), fetched with one shuffle per register.
-template <int VW>
+template <int VW, bool PLAIN>
 __global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, float *__restrict__ x,
                                                                const float *__restrict__ r, float *__restrict__ p,
                                                                float2 *__restrict__ T1,
@@ -331,8 +331,10 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, flo
     const int rr = i >> 5, c = i & 31;
     twl[rr * 32 + (c >> 1) + 16 * (c & 1)] = tw1024[i];
   }
+  // PLAIN (y = G x): p is the input x, nothing is updated
   float be = 0.f, al = 0.f;
   auto scalars = [&]() {
+    if (PLAIN) return;
     const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
     double beta = 0.0, alpha_prev = 0.0;
     if (k > 0) {
@@ -363,8 +365,10 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, flo
       if (ok[u]) {
         const size_t e = so + (size_t)rr * N + j;
         vload<float, VW>(pv[u], p + e);
-        vload<float, VW>(rv[u], r + e);
-        vload<float, VW>(xv[u], x + e);
+        if (!PLAIN) {
+          vload<float, VW>(rv[u], r + e);
+          vload<float, VW>(xv[u], x + e);
+        }
       }
     }
     if (i0 == (int)threadIdx.x) scalars();  // first batch: uniform across the CTA
@@ -373,14 +377,16 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, flo
       const int i = i0 + u * NT;
       const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
       if (ok[u]) {
-        const size_t e = so + (size_t)rr * N + j;
+        if (!PLAIN) {
+          const size_t e = so + (size_t)rr * N + j;
 #pragma unroll
-        for (int c = 0; c < VW; ++c) {
-          xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
-          pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+          for (int c = 0; c < VW; ++c) {
+            xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
+            pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+          }
+          vstore<float, VW>(x + e, xv[u]);
+          vstore<float, VW>(p + e, pv[u]);
         }
-        vstore<float, VW>(x + e, xv[u]);
-        vstore<float, VW>(p + e, pv[u]);
       } else {
 #pragma unroll
         for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
@@ -975,13 +981,13 @@ static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx
       constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * 17;
       static_assert(sm >= sizeof(float) * 32 * 264 && sm >= sizeof(float2) * 16 * 32 * 17, "pass A 512 smem");
       if (can_vec<T>(N, x, r, p)) {
-        cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<4>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<4, false>, sm);
         if (e != cudaSuccess) return e;
-        cg_pass_a_512_kernel<4><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_512_kernel<4, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
       } else {
-        cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<1>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<1, false>, sm);
         if (e != cudaSuccess) return e;
-        cg_pass_a_512_kernel<1><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_512_kernel<1, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, twl, w);
       }
       return cudaGetLastError();
     }
@@ -1081,12 +1087,29 @@ cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork
   return cudaGetLastError();
 }
 
-// y = G x with the warp-FFT passes (FP32, L = 1024): pass A in PLAIN mode (x -> T1), pass B
+// y = G x with the warp-FFT passes (FP32, L = 512 or 1024): pass A in PLAIN mode (x -> T1), pass B
 // (normal.cu), pass C in MODE 3 (T1 -> y).  Returns cudaErrorNotSupported otherwise.
 cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaStream_t s) {
-  if (L != 1024 || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  if ((L != 1024 && L != 512) || !pass_c_warp_enabled()) return cudaErrorNotSupported;
   const float2 *twl = tw1024_table();
   if (!twl) return cudaErrorMemoryAllocation;
+  if (L == 512) {
+    constexpr size_t sm5 = sizeof(float4) * (512 / 2 + 1) * 17;
+    FusedWork w{};
+    w.nparts = fused_parts(N, L, true);
+    w.B = B;
+    float *xp = const_cast<float *>(x);
+    if (can_vec<float>(N, x, nullptr, nullptr)) {
+      cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<4, true>, sm5);
+      if (e != cudaSuccess) return e;
+      cg_pass_a_512_kernel<4, true><<<dim3(w.nparts, B), 256, sm5, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
+    } else {
+      cudaError_t e = cg_set_smem(cg_pass_a_512_kernel<1, true>, sm5);
+      if (e != cudaSuccess) return e;
+      cg_pass_a_512_kernel<1, true><<<dim3(w.nparts, B), 256, sm5, s>>>(N, 0, nullptr, nullptr, xp, T1, twl, w);
+    }
+    return cudaGetLastError();
+  }
   constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * (WROWS / 2 + 1);
   FusedWork w{};
   w.nparts = fused_parts(N, L, true);
@@ -1104,9 +1127,19 @@ cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaSt
   return cudaGetLastError();
 }
 cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaStream_t s) {
-  if (L != 1024 || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  if ((L != 1024 && L != 512) || !pass_c_warp_enabled()) return cudaErrorNotSupported;
   const float2 *twl = tw1024_table();
   if (!twl) return cudaErrorMemoryAllocation;
+  if (L == 512) {
+    constexpr size_t sm5 = sizeof(float4) * (512 / 2 + 1) * 17;
+    FusedWork w{};
+    w.nparts = fused_parts(N, L, true);
+    w.B = B;
+    cudaError_t e = cg_set_smem(cg_pass_c_512_kernel<3>, sm5);
+    if (e != cudaSuccess) return e;
+    cg_pass_c_512_kernel<3><<<dim3(w.nparts, B), 256, sm5, s>>>(N, 0, 0, T1, nullptr, y, twl, w);
+    return cudaGetLastError();
+  }
   constexpr size_t sm = sizeof(float4) * (1024 / 2 + 1) * (WROWS / 2 + 1);
   FusedWork w{};
   w.nparts = fused_parts(N, L, true);
