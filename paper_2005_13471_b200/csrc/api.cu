@@ -425,6 +425,7 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     }
   if (!p->cap) CU(cudaStreamCreateWithFlags(&p->cap, cudaStreamNonBlocking));
   (void)tw1024_table();  // any lazy device allocation happens before capture
+  (void)tw2048_table();
   CU(cudaStreamBeginCapture(p->cap, cudaStreamCaptureModeThreadLocal));
   p->launches = 0;
   bsct_status st = solve_launch_t<T>(p, b, x, B, iters, solver, resid, flags, p->cap);
