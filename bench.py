@@ -461,6 +461,28 @@ def run_ours(args):
                  "note": "8 angle shards built back to back on one GPU (a rank's compute before the NCCL "
                          "allreduce of the 16.8 MB partial filter, which is not measured here)"}
         del t4, part, acc
+        # D6: back projection of one config-4 slice, whole vs 8 angle shards (plans on the
+        # sub-geometries); a rank's compute before the 4 MB allreduce of its partial image
+        from paper_2005_13471_b200.parallel import angle_shard_geometry
+        taps4 = torch.zeros((2 * N4 - 1, 2 * N4 - 1), device=dev)
+        taps4[N4 - 1, N4 - 1] = 1.0  # the back projection does not read the filter
+        s4 = torch.rand((1, na, CONFIGS[4].n_det), device=dev, generator=torch.Generator(device=dev).manual_seed(4))
+        b4 = torch.empty((1, N4, N4), device=dev)
+        pl4 = bsct.plan_create(g4, taps4, max_batch=1)
+        bp_full = timed(lambda: bsct.backproject(pl4, s4, b4))
+        pb4, acc4, bp_shard = torch.empty_like(b4), torch.zeros_like(b4), []
+        for r in range(8):
+            sub, lo, hi = angle_shard_geometry(g4, 8, r)
+            pls = bsct.plan_create(sub, taps4, max_batch=1)
+            ss = s4[:, lo:hi].contiguous()
+            bp_shard.append(timed(lambda: bsct.backproject(pls, ss, pb4)))
+            acc4 += pb4
+        gram4["backproject_angle_shards"] = {
+            "full_ms": bp_full, "shard8_ms_max": max(bp_shard),
+            "shard8_sum_rel_diff": float((acc4 - b4).norm() / b4.norm()),
+            "note": "one 1024^2 slice, 720 angles (SURVEY.md D6, parallel.backproject_sharded); the 4 MB "
+                    "allreduce is not measured on one GPU"}
+        del taps4, s4, b4, pb4, acc4
 
     # ---- NEXT-1 (side measurement): forward projector H, plain adjoint H^T and one SIRT
     # iteration on 256 of the slices, against one filter-based CG iteration on the same slices

@@ -7,6 +7,11 @@ Only where the path shards:
   gram_build_sharded -- config 4: each rank builds the partial Gram filter over its angle
                      range (bsct_gram_build(angle_begin, angle_end), P:96-129 is a sum over
                      angles) and the partials are summed by one allreduce over NVLink.
+* angle_shard_geometry /
+  backproject_sharded -- one large slice: the back projection
+                     b = H^T g is also a sum over angles, so each rank back projects
+                     its angle range with a plan built on the sub-geometry and one allreduce of
+                     the N^2 partial image (4 MB at N = 1024) sums them.
 """
 from __future__ import annotations
 
@@ -43,3 +48,29 @@ def gram_build_sharded(geom: dict, taps, group=None, stream=None):
     a0, a1 = angle_shard(len(geom["angles"]), world, rank)
     gram_build(geom, taps, a0, a1, stream=stream)
     return allreduce_taps(taps, group)
+
+
+def angle_shard_geometry(geom: dict, world: int, rank: int) -> tuple[dict, int, int]:
+    """This rank's sub-geometry (angles[a0:a1], everything else unchanged) and [a0, a1)."""
+    a0, a1 = angle_shard(len(geom["angles"]), world, rank)
+    sub = dict(geom)
+    sub["angles"] = list(geom["angles"])[a0:a1]
+    return sub, a0, a1
+
+
+def backproject_sharded(plan_shard, sino_shard, b, group=None, stream=None):
+    """Full back projection b[B, N, N] of a sinogram whose angles are split over the ranks:
+    this rank's partial H^T g over its angle range (plan_shard built on
+    angle_shard_geometry(...)[0], sino_shard = sino[:, a0:a1, :]), then allreduce(SUM).
+    plan_shard None (an empty angle range when world > n_angles) contributes zeros."""
+    import torch.distributed as dist
+
+    from . import backproject
+    if plan_shard is None:
+        b.zero_()
+    else:
+        backproject(plan_shard, sino_shard, b, stream=stream)
+    if stream is not None:
+        stream.synchronize()
+    dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
+    return b

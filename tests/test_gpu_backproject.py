@@ -153,3 +153,48 @@ def test_v3_slices_per_cta(cuda_lib, ci, B, sb, monkeypatch):
     k1, k2 = rng.integers(0, N, 200), rng.integers(0, N, 200)
     ref = backproject(g, sino[B - 1], pixels=(k1, k2))
     assert rel_l2(b3[B - 1][k1, k2], ref) < 1e-5
+
+
+def test_angle_sharded_backprojection(cuda_lib):
+    """the back projection of one large slice split over angle shards (plans on
+    parallel.angle_shard_geometry sub-geometries) sums to the whole-geometry back projection;
+    parallel.backproject_sharded end to end on a one-rank NCCL group; sampled pixels of the
+    sum against the oracle."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_13471_b200.parallel import angle_shard_geometry, backproject_sharded
+    N, n, M = 300, 90, 425
+    g = dict(N=N, lambda_x=1.0, angles=list(np.arange(n) * np.pi / n + 0.02), lambda_y=1.0, n_det=M, zeta=1.0)
+    taps = torch.zeros((2 * N - 1, 2 * N - 1), device="cuda")
+    taps[N - 1, N - 1] = 1.0  # the back projection does not use the filter
+    rng = np.random.default_rng(66)
+    sino = rng.uniform(0, 1, (1, n, M))
+    sd = to_dev(sino, "f32")
+    full = torch.empty((1, N, N), device="cuda")
+    cuda_lib.backproject(cuda_lib.plan_create(g, taps, max_batch=1), sd, full)
+    acc = torch.zeros_like(full)
+    part = torch.empty_like(full)
+    for r in range(3):
+        sub, a0, a1 = angle_shard_geometry(g, 3, r)
+        cuda_lib.backproject(cuda_lib.plan_create(sub, taps, max_batch=1), sd[:, a0:a1].contiguous(), part)
+        acc += part
+    torch.cuda.synchronize()
+    assert rel_l2(to_np(acc), to_np(full)) < 1e-6
+    k1, k2 = rng.integers(0, N, 60), rng.integers(0, N, 60)
+    assert rel_l2(to_np(acc[0])[k1, k2], backproject(g, sino[0], pixels=(k1, k2))) < 1e-5
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        sub, a0, a1 = angle_shard_geometry(g, 1, 0)
+        out = torch.empty_like(full)
+        backproject_sharded(cuda_lib.plan_create(sub, taps, max_batch=1), sd[:, a0:a1].contiguous(), out)
+        torch.cuda.synchronize()
+        assert torch.equal(out, full)
+    finally:
+        dist.destroy_process_group()

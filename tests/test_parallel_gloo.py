@@ -1,6 +1,7 @@
 """World-size-2 gloo tests (CPU) of the multi-GPU plumbing: slice shards cover every slice
-once, and angle-sharded partial Gram filters allreduced with the product's collective
-equal the full filter (partials computed by the oracle here, by K1 on the GPU box)."""
+once, angle-sharded partial Gram filters allreduced with the product's collective equal the
+full filter, and angle-sharded partial back projections allreduced equal the
+full back projection (partials computed by the oracle here, by K1 / K4 on the GPU box)."""
 import os
 import socket
 
@@ -10,7 +11,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2005_13471_b200.parallel import allreduce_taps, angle_shard, slice_shard
+from paper_2005_13471_b200.parallel import allreduce_taps, angle_shard, angle_shard_geometry, slice_shard
 
 
 def test_shards_partition():
@@ -70,3 +71,38 @@ def test_gloo_angle_shards_allreduce():
     g = dict(N=12, lambda_x=1.0, angles=np.arange(30) * np.pi / 30, lambda_y=0.5, n_det=49, zeta=0.5)
     assert np.abs(taps - gram_taps(g)).max() < 1e-13
     assert (cover == 1).all()
+
+
+G6 = dict(N=10, lambda_x=1.0, angles=list(np.arange(25) * np.pi / 25 + 0.05), lambda_y=0.75, n_det=31, zeta=1.0)
+
+
+def _bp_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle.backproject import backproject
+    sino = np.random.default_rng(6).uniform(0, 1, (25, 31))
+    sub, a0, a1 = angle_shard_geometry(G6, world, rank)
+    assert len(sub["angles"]) == a1 - a0 and sub["N"] == G6["N"]
+    part = torch.tensor(backproject(sub, sino[a0:a1]))
+    dist.all_reduce(part)  # the collective of parallel.backproject_sharded
+    if rank == 0:
+        out.put(part.numpy())
+    dist.destroy_process_group()
+
+
+def test_gloo_angle_sharded_backprojection():
+    from oracle.backproject import backproject
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_bp_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    b = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    sino = np.random.default_rng(6).uniform(0, 1, (25, 31))
+    ref = backproject(G6, sino)
+    assert np.abs(b - ref).max() < 1e-12 * np.abs(ref).max()
