@@ -202,73 +202,72 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
 }
 
 // ---------------------------------------------------------------- pass B, L = 2048 (FP32)
-// One warp per column, 64 x 32 four-step FFT split by the parity e of the first-stage index:
-// lane t holds x[t + 32 r] (r < 32: rows >= N <= 1024 are zero), and for e = 0, 1
+// Two warps per column, 64 x 32 four-step FFT split by the parity e of the first-stage index:
+// lane t holds x[t + 32 r] (r < 32: rows >= N <= 1024 are zero), and warp e = 0, 1 computes
 //   v[m] = DFT_32 over r of x_r W_64^{r e}          (= Y[2m + e], the half-input DFT_64)
 //   * W_2048^{t (2m + e)}, transpose, DFT_32 over t  -> X[2 lane + e + 64 k]
 //   * S, Parseval, and the same steps backwards, ending in
-//   z[t + 32 r] += W_64^{-r e} IDFT_32 over m of U[2m + e][t]
-// so only 32 complex values per lane are live; the e = 0 half of z waits in shared memory
-// (the column still holds x for the e = 1 half).  Twiddles come from tw2048_table() through
-// L1: [e][m][t] = W_2048^{(2m + e) t} (forward, coalesced over t) and [2 + e][t][m] (inverse,
+//   z_e[t + 32 r] = W_64^{-r e} IDFT_32 over m of U[2m + e][t]
+// so only 32 complex values per lane are live; warp 1 hands z_1 to warp 0 through shared
+// memory, which stores z_0 + z_1.  Twiddles come from tw2048_table() through L1:
+// [e][m][t] = W_2048^{(2m + e) t} (forward, coalesced over t) and [2 + e][t][m] (inverse,
 // coalesced over m).
-constexpr int PB2_WARPS = 4;
+constexpr int PB2_COLS = 2;  // columns per CTA (2 warps each)
 
 template <bool FULL>
-__global__ void __launch_bounds__(PB2_WARPS * 32, 3) pass_b_2048_kernel(int N, float2 *__restrict__ T1,
-                                                                      const float *__restrict__ S,
-                                                                      const float2 *__restrict__ tw2,
-                                                                      double *__restrict__ gpart) {
-  constexpr int L = 2048, Q = L / 2 + 1;
-  extern __shared__ __align__(16) float2 pb2_smem[];  // [PB2_WARPS][32 * 33] transposes, [PB2_WARPS][32 * 32] z0
-  __shared__ double red[PB2_WARPS];
+__global__ void __launch_bounds__(PB2_COLS * 64, 4) pass_b_2048_kernel(int N, float2 *__restrict__ T1,
+                                                                     const float *__restrict__ S,
+                                                                     const float2 *__restrict__ tw2,
+                                                                     double *__restrict__ gpart) {
+  constexpr int L = 2048, Q = L / 2 + 1, NWP = 2 * PB2_COLS;
+  extern __shared__ __align__(16) float2 pb2_smem[];  // [NWP][32 * 33] transposes, [PB2_COLS][32 * 32] z_1
+  __shared__ double red[NWP];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = warp >> 1, e = warp & 1;
   const int b = blockIdx.y;
-  const int q0 = blockIdx.x * PB2_WARPS + warp;
+  const int q0 = blockIdx.x * PB2_COLS + c;
   const bool live = q0 < Q;  // warps past the last column recompute column Q - 1, store nothing
   const int q = live ? q0 : Q - 1;
   float2 *col = T1 + ((size_t)b * Q + q) * N;
-  float2 *tr = pb2_smem + warp * (32 * 33), *z0 = pb2_smem + PB2_WARPS * (32 * 33) + warp * (32 * 32);
-  const float *Sq = S + (size_t)q * L + 2 * lane;
+  float2 *tr = pb2_smem + warp * (32 * 33), *zx = pb2_smem + NWP * (32 * 33) + c * (32 * 32);
+  const float *Sq = S + (size_t)q * L + 2 * lane + e;
+  const float2 *twf = tw2 + e * 1024, *twi = tw2 + (2 + e) * 1024;
+  float2 v[32];
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    const int n = lane + 32 * r;
+    const float2 xv = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
+    v[r] = (e && r) ? cmul(xv, __ldg(tw2 + 16 * 32 + r)) : xv;  // W_64^r = W_2048^{32 r}
+  }
+  dft32<false>(v);  // v[m] = Y[2m + e]
+#pragma unroll
+  for (int m = 0; m < 32; ++m)
+    if (e || m) v[m] = cmul(v[m], __ldg(twf + m * 32 + lane));  // W_2048^{(2m + e) t}
+  warp_transpose32(v, tr, lane);  // lane m: v[t]
+  dft32<false>(v);                // v[k] = X[2 lane + e + 64 k]
   float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll 1
-  for (int e = 0; e < 2; ++e) {
-    const float2 *twf = tw2 + e * 1024, *twi = tw2 + (2 + e) * 1024;
-    float2 v[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) {
+    const float2 w = cscale(v[k], Sq[64 * k]);
+    g2[k & 1] = cfma2(w, v[k], g2[k & 1]);
+    v[k] = w;
+  }
+  dft32<true>(v);  // over k: v[t] = U[2 lane + e][t]
+#pragma unroll
+  for (int t = 0; t < 32; ++t)
+    if (e || t) v[t] = cmulc(v[t], __ldg(twi + t * 32 + lane));  // W_2048^{(2 lane + e) t}
+  warp_transpose32(v, tr, lane);  // lane t: v[m] = U[2m + e][t]
+  dft32<true>(v);                 // v[r] = sum_m U[2m + e][t] W_32^{-r m}
+  if (e) {
+#pragma unroll
+    for (int r = 0; r < 32; ++r) zx[r * 32 + lane] = r ? cmulc(v[r], __ldg(tw2 + 16 * 32 + r)) : v[r];
+  }
+  __syncthreads();
+  if (!e) {
 #pragma unroll
     for (int r = 0; r < 32; ++r) {
       const int n = lane + 32 * r;
-      const float2 xv = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
-      v[r] = (e && r) ? cmul(xv, __ldg(tw2 + 16 * 32 + r)) : xv;  // W_64^r = W_2048^{32 r}
-    }
-    dft32<false>(v);  // v[m] = Y[2m + e]
-#pragma unroll
-    for (int m = 0; m < 32; ++m)
-      if (e || m) v[m] = cmul(v[m], __ldg(twf + m * 32 + lane));  // W_2048^{(2m + e) t}
-    warp_transpose32(v, tr, lane);  // lane m: v[t]
-    dft32<false>(v);                // v[k] = X[2 lane + e + 64 k]
-#pragma unroll
-    for (int k = 0; k < 32; ++k) {
-      const float2 w = cscale(v[k], Sq[e + 64 * k]);
-      g2[k & 1] = cfma2(w, v[k], g2[k & 1]);
-      v[k] = w;
-    }
-    dft32<true>(v);  // over k: v[t] = U[2 lane + e][t]
-#pragma unroll
-    for (int t = 0; t < 32; ++t)
-      if (e || t) v[t] = cmulc(v[t], __ldg(twi + t * 32 + lane));  // W_2048^{(2 lane + e) t}
-    warp_transpose32(v, tr, lane);  // lane t: v[m] = U[2m + e][t]
-    dft32<true>(v);                 // v[r] = sum_m U[2m + e][t] W_32^{-r m}
-    if (e == 0) {
-#pragma unroll
-      for (int r = 0; r < 32; ++r) z0[r * 32 + lane] = v[r];
-    } else {
-#pragma unroll
-      for (int r = 0; r < 32; ++r) {
-        const int n = lane + 32 * r;
-        const float2 zr = cadd(z0[r * 32 + lane], r ? cmulc(v[r], __ldg(tw2 + 16 * 32 + r)) : v[r]);
-        if (live && (FULL || n < N)) col[n] = zr;
-      }
+      if (live && (FULL || n < N)) col[n] = cadd(v[r], zx[r * 32 + lane]);
     }
   }
   double gam = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
@@ -280,7 +279,7 @@ __global__ void __launch_bounds__(PB2_WARPS * 32, 3) pass_b_2048_kernel(int N, f
     __syncthreads();
     if (threadIdx.x == 0) {
       double t = 0;
-      for (int i = 0; i < PB2_WARPS; ++i) t += red[i];
+      for (int i = 0; i < NWP; ++i) t += red[i];
       gpart[(size_t)b * gridDim.x + blockIdx.x] = t;
     }
   }
@@ -616,15 +615,15 @@ static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T>
     if (pass_b_warp_enabled()) {
       const float2 *tw2 = tw2048_table();
       if (!tw2) return cudaErrorMemoryAllocation;
-      const dim3 grid((L / 2 + 1 + PB2_WARPS - 1) / PB2_WARPS, B);
-      constexpr size_t sm = sizeof(float2) * PB2_WARPS * (32 * 33 + 32 * 32);
+      const dim3 grid((L / 2 + 1 + PB2_COLS - 1) / PB2_COLS, B);
+      constexpr size_t sm = sizeof(float2) * (2 * PB2_COLS * 32 * 33 + PB2_COLS * 32 * 32);
       cudaError_t e = set_smem(pass_b_2048_kernel<true>, sm);
       if (e == cudaSuccess) e = set_smem(pass_b_2048_kernel<false>, sm);
       if (e != cudaSuccess) return e;
       if (N == L / 2)
-        pass_b_2048_kernel<true><<<grid, PB2_WARPS * 32, sm, s>>>(N, T1, S, tw2, gpart);
+        pass_b_2048_kernel<true><<<grid, PB2_COLS * 64, sm, s>>>(N, T1, S, tw2, gpart);
       else
-        pass_b_2048_kernel<false><<<grid, PB2_WARPS * 32, sm, s>>>(N, T1, S, tw2, gpart);
+        pass_b_2048_kernel<false><<<grid, PB2_COLS * 64, sm, s>>>(N, T1, S, tw2, gpart);
       return cudaGetLastError();
     }
   }
@@ -679,7 +678,7 @@ bool pass_b_warp_enabled() {
 int pass_b_blocks(int L, bool fp32) {
   if (fp32 && L == 1024 && pass_b_warp_enabled()) return (1024 / 2 + 1 + PB_WARPS - 1) / PB_WARPS;  // FP32 warp kernel
   if (fp32 && L == 512 && pass_b_warp_enabled()) return (512 / 2 + 1 + 2 * PB5_WARPS - 1) / (2 * PB5_WARPS);
-  if (fp32 && L == 2048 && pass_b_warp_enabled()) return (2048 / 2 + 1 + PB2_WARPS - 1) / PB2_WARPS;
+  if (fp32 && L == 2048 && pass_b_warp_enabled()) return (2048 / 2 + 1 + PB2_COLS - 1) / PB2_COLS;
   switch (L) {
     case 2: return (2 / 2 + 1 + FftLaunchB<2>::G - 1) / FftLaunchB<2>::G;
     case 4: return (4 / 2 + 1 + FftLaunchB<4>::G - 1) / FftLaunchB<4>::G;
