@@ -22,6 +22,7 @@
 namespace bsct {
 
 const float2 *tw1024_table();  // normal.cu: W_1024^{jt}, [32][32]
+const float2 *tw2048_table();  // normal.cu: W_2048^{(2m+e)t}, [4][32][32]
 bool pass_c_warp_enabled();
 bool bulk_stage_enabled();  // BSCT_BULK=1: bulk (TMA) copies instead of cp.async staging
 
@@ -864,6 +865,138 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_512_kernel(int N, int k, int
   if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
 }
 
+// ---------------------------------------------------------------- pass C, L = 2048 (FP32 warp FFTs)
+// Same contract as cg_pass_c_kernel<float, 2048> (8 rows per CTA = the generic pass A's
+// partition).  T1[q][row0 .. row0 + 8) staged by cp.async as [q parity][q / 2][5] row-pair
+// float4 slots (a warp only reads one parity of q, so consecutive lanes hit consecutive slots);
+// two warps per row pair run the inverse of pass_b_2048_kernel's parity split: warp e takes
+// Z[2m + e + 64 k] (lane m), IDFT_32 over k, conj W_2048^{(2m + e) t}, transpose, IDFT_32 over
+// m, * W_64^{-r e}; the two warps swap halves through their transpose buffers and warp e
+// updates r (and x) of row a (e = 0) or b (e = 1) of the pair (z = y_a + i y_b, outputs r < 32
+// only: N <= 1024), its r row prefetched into registers before the FFT.
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) cg_pass_c_2048_kernel(int N, int k, int gparts, const float2 *__restrict__ T1,
+                                                                float *__restrict__ x, float *__restrict__ r,
+                                                                const float2 *__restrict__ tw2, FusedWork w) {
+  constexpr int L = 2048, Q = L / 2 + 1, ROWS = 8, NP = ROWS / 2, RS = NP + 1, HALF = L / 4 + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [2][HALF][RS], later [8][32][33] float2
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, e = warp & 1;
+  const int b = blockIdx.y;
+  const int row0 = blockIdx.x * ROWS;
+  const int rows = min(ROWS, N - row0);
+  const float2 *T1s = T1 + (size_t)b * Q * N + row0;
+  auto slot = [&](int q) { return st + ((q & 1) * HALF + (q >> 1)) * RS; };
+  for (int i = threadIdx.x; i < Q * NP; i += blockDim.x) {
+    const int q = i / NP, pr = i % NP, rp = 2 * pr;
+    float4 *dst = slot(q) + pr;
+    const float2 *src = T1s + (size_t)q * N + rp;
+    if (rp + 1 < rows) {
+      if (!(N & 1)) {
+        cp_async16_g(dst, src);
+      } else {
+        cp_async8_g(dst, src);
+        cp_async8_g(reinterpret_cast<float2 *>(dst) + 1, src + 1);
+      }
+    } else if (rp < rows) {
+      cp_async8_g(dst, src);
+      reinterpret_cast<float2 *>(dst)[1] = float2{0.f, 0.f};
+    } else {
+      *dst = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+  asm volatile("cp.async.commit_group;\n" ::);
+  double rho = 0.0;
+  if (MODE == 3) {
+  } else if (MODE == 0) {
+    rho = w.rho[(size_t)b * w.rho_stride + k];
+  } else {
+    rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+  }
+  double alpha = 0.0;
+  if (MODE == 3) {
+  } else if (MODE == 2) {
+    alpha = *w.tau;
+  } else {
+    const double gam = cta_reduce_parts(w.gpart + (size_t)b * gparts, gparts, red);
+    const bool bad = rho > 0 && !(gam > 0);
+    const bool frozen = bad || (w.flags && w.flags[b]);
+    alpha = (rho > 0 && !frozen) ? rho / gam : 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
+  }
+  if (MODE != 3 && blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
+  const float al = (float)alpha;
+  // this warp's row (a for e = 0, b for e = 1) of r into registers: latency overlaps the FFT
+  const int row = row0 + 2 * pair + e;
+  const bool hr = row < N;
+  float *rw = r + ((size_t)b * N + row) * N, *xw = x + ((size_t)b * N + row) * N;
+  float rv[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int n = lane + 32 * m;
+    rv[m] = (MODE != 3 && hr && n < N) ? rw[n] : 0.f;
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::);
+  __syncthreads();
+  // Z[q] = X_a[q] + i X_b[q] (q <= 1024), Z[L - q] = conj X_a[q] + i conj X_b[q]
+  float2 v[32];
+#pragma unroll
+  for (int kk = 0; kk < 32; ++kk) {
+    const int qq = 2 * lane + e + 64 * kk;
+    if (kk < 16 || (kk == 16 && qq == L / 2)) {
+      float4 c = slot(qq)[pair];
+      if (qq == 0 || qq == L / 2) { c.y = 0.f; c.w = 0.f; }  // DC / Nyquist of real rows
+      v[kk] = float2{c.x - c.w, c.y + c.z};
+    } else {
+      const float4 c = slot(L - qq)[pair];
+      v[kk] = float2{c.x + c.w, c.z - c.y};
+    }
+  }
+  dft32<true>(v);  // over k: v[t] = U[2 lane + e][t]
+  const float2 *twi = tw2 + (2 + e) * 1024;
+#pragma unroll
+  for (int t = 0; t < 32; ++t)
+    if (e || t) v[t] = cmulc(v[t], __ldg(twi + t * 32 + lane));  // W_2048^{(2 lane + e) t}
+  __syncthreads();  // staging area becomes the transpose buffers
+  float2 *tr = reinterpret_cast<float2 *>(smem_raw) + warp * (32 * 33);
+  warp_transpose32(v, tr, lane);  // lane t: v[m] = U[2m + e][t]
+  dft32<true>(v);                 // v[rr] = sum_m U[2m + e][t] W_32^{-rr m}
+  if (e) {
+#pragma unroll
+    for (int rr = 1; rr < 32; ++rr) v[rr] = cmulc(v[rr], __ldg(tw2 + 16 * 32 + rr));  // W_64^{-rr}
+  }
+#pragma unroll
+  for (int rr = 0; rr < 32; ++rr) tr[rr * 32 + lane] = v[rr];  // hand this half to the other warp
+  __syncthreads();
+  const float2 *zo = reinterpret_cast<float2 *>(smem_raw) + (warp ^ 1) * (32 * 33);
+  float ac = 0.f;
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const int n = lane + 32 * m;
+    if (hr && n < N) {
+      const float2 z = cadd(v[m], zo[m * 32 + lane]);  // z_0 + z_1 = y_a + i y_b at n
+      const float zv = e ? z.y : z.x;
+      if (MODE == 3) {  // y = G x into the r pointer
+        rw[n] = zv;
+        continue;
+      }
+      if (MODE != 0) xw[n] = fmaf(al, rv[m], xw[n]);
+      const float tv = fmaf(-al, zv, rv[m]);
+      rw[n] = tv;
+      ac = fmaf(tv, tv, ac);
+    }
+  }
+  if (MODE == 3) return;
+  const double s = cta_sum((double)ac, red);
+  if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
+}
+
 // ---------------------------------------------------------------- final: rho_K, resid, CG x update
 template <typename T>
 __global__ void __launch_bounds__(256) cg_final_kernel(long n, int K, int cg, T *__restrict__ x,
@@ -1021,6 +1154,19 @@ static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *
       return cudaGetLastError();
     }
   }
+  if constexpr (std::is_same<T, float>::value && L == 2048) {
+    static_assert(2 * FftLaunch<2048>::G == 8, "cg_pass_c_2048_kernel covers the generic pass A's 8-row partition");
+    if (pass_c_warp_enabled()) {
+      const float2 *tw2 = tw2048_table();
+      if (!tw2) return cudaErrorMemoryAllocation;
+      constexpr size_t sm = sizeof(float4) * 2 * (L / 4 + 1) * 5;
+      static_assert(sm >= sizeof(float2) * 8 * 32 * 33, "pass C 2048 smem");
+      cudaError_t e = cg_set_smem(cg_pass_c_2048_kernel<MODE>, sm);
+      if (e != cudaSuccess) return e;
+      cg_pass_c_2048_kernel<MODE><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, gparts, T1, x, r, tw2, w);
+      return cudaGetLastError();
+    }
+  }
   if constexpr (std::is_same<T, float>::value && L == 512) {
     static_assert(2 * FftLaunch<512>::G == 32, "cg_pass_c_512_kernel covers the generic pass A's 32-row partition");
     if (pass_c_warp_enabled()) {
@@ -1127,7 +1273,19 @@ cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaSt
   return cudaGetLastError();
 }
 cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaStream_t s) {
-  if ((L != 1024 && L != 512) || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  if ((L != 1024 && L != 512 && L != 2048) || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  if (L == 2048) {
+    const float2 *tw2 = tw2048_table();
+    if (!tw2) return cudaErrorMemoryAllocation;
+    constexpr size_t sm2 = sizeof(float4) * 2 * (2048 / 4 + 1) * 5;
+    FusedWork w{};
+    w.nparts = fused_parts(N, L, true);
+    w.B = B;
+    cudaError_t e = cg_set_smem(cg_pass_c_2048_kernel<3>, sm2);
+    if (e != cudaSuccess) return e;
+    cg_pass_c_2048_kernel<3><<<dim3(w.nparts, B), 256, sm2, s>>>(N, 0, 0, T1, nullptr, y, tw2, w);
+    return cudaGetLastError();
+  }
   const float2 *twl = tw1024_table();
   if (!twl) return cudaErrorMemoryAllocation;
   if (L == 512) {

@@ -28,7 +28,7 @@ def check_apply(bsct, g, dt, B, seed, direct=False):
 @pytest.mark.parametrize("N,n,zeta,dt,B", [
     (1, 4, 0.0, "f32", 2), (2, 5, 1.0, "f32", 3), (3, 6, 0.5, "f64", 2), (5, 9, 1.0, "f32", 3),
     (8, 12, 0.0, "f32", 1), (13, 20, 1.0, "f64", 2), (24, 30, 1.0, "f32", 2), (37, 40, 0.5, "f32", 3),
-    (100, 60, 1.0, "f32", 2), (129, 64, 1.0, "f32", 1), (200, 50, 1.0, "f32", 2), (256, 45, 0.0, "f32", 3), (257, 30, 0.5, "f32", 2), (300, 40, 1.0, "f32", 1)])
+    (100, 60, 1.0, "f32", 2), (129, 64, 1.0, "f32", 1), (200, 50, 1.0, "f32", 2), (256, 45, 0.0, "f32", 3), (257, 30, 0.5, "f32", 2), (300, 40, 1.0, "f32", 1), (701, 24, 1.0, "f32", 2)])
 def test_small_and_ragged(cuda_lib, N, n, zeta, dt, B):
     check_apply(cuda_lib, geom(N, uniform(n), 2 * N + 1, zeta=zeta), dt, B, seed=N, direct=N <= 24)
 

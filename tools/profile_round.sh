@@ -16,3 +16,11 @@ echo "full rc=$?"
 # K4 separately (its first launches would be skipped above)
 ncu --set full --clock-control none --import-source on -k regex:bp_v3 -s 1 -c 1 -o $O/prof_bp $CMD2 > $O/ncu_bp.log 2>&1
 echo "bp rc=$?"
+# summaries on the box (gpurun copies back at most 64 MiB of gpurun_out/)
+python tools/ncu_summary.py $O/prof_full.ncu-rep > $O/ncu_full_summary.txt 2>&1
+python tools/ncu_summary.py $O/prof_bp.ncu-rep | tail -n +2 >> $O/ncu_full_summary.txt 2>&1
+python tools/ncu_traffic.py $O/prof_full.ncu-rep 64 > $O/ncu_traffic_full.json 2>&1
+python tools/ncu_traffic.py $O/prof_bp.ncu-rep 64 > $O/ncu_traffic_bp.json 2>&1
+python tools/launch_shares.py $O/launches.csv > $O/launch_shares.txt 2>&1
+gzip -f $O/launches.csv
+rm -f $O/prof_full.ncu-rep
