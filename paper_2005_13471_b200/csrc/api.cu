@@ -333,10 +333,10 @@ template <typename T>
 bsct_status normal_apply_t(bsct_plan p, const T *x, T *y, int B, double *gpart, cudaStream_t s) {
   auto *T1 = (cplx<T> *)p->T1;
   auto *tw = (const cplx<T> *)p->tw;
-  // warp-level passes: A at L = 512 / 1024, C at L = 512 / 1024 / 2048 (pass B dispatches itself)
-  const bool fp32 = std::is_same<T, float>::value && pass_c_warp_enabled();
-  const bool warp = fp32 && (p->L == 1024 || p->L == 512);
-  const bool warpc = warp || (fp32 && p->L == 2048);
+  // warp-level passes A and C at L = 512 / 1024 / 2048 (pass B dispatches itself)
+  const bool warp = std::is_same<T, float>::value && pass_c_warp_enabled() &&
+                    (p->L == 1024 || p->L == 512 || p->L == 2048);
+  const bool warpc = warp;
   if (warp)
     LAUNCH(p, BSCT_K_PASS_A, 1, (warp_apply_a(p->N, p->L, B, (const float *)x, (float2 *)T1, s)));
   else

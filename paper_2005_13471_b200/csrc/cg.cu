@@ -461,6 +461,142 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, flo
   }
 }
 
+// ---------------------------------------------------------------- pass A (CG), L = 2048 (FP32 warp FFTs)
+// Same contract as cg_pass_a_kernel<float, 2048> (8 rows per CTA).  Streaming phase as in
+// cg_pass_a_1024_kernel (new p rows in shared memory, stride 1032 floats); two warps per row
+// pair run pass_b_2048_kernel's parity-split forward FFT of z = p_a + i p_b: warp e ends with
+// Z[2m + e + 64 k] in lane m, register k, whose Hermitian partner Z[L - q] has the same parity:
+// lane (32 - m) mod 32, register 31 - k for e = 0 (lane 0: its own register (32 - k) mod 32) and
+// lane 31 - m, register 31 - k for e = 1 -- one shuffle per register.  T1[q][row0 .. row0 + 8)
+// is written through a [q parity][q / 2][5] float4 staging tile (64 contiguous bytes per q).
+template <int VW, bool PLAIN>
+__global__ void __launch_bounds__(256, 2) cg_pass_a_2048_kernel(int N, int k, float *__restrict__ x,
+                                                                const float *__restrict__ r, float *__restrict__ p,
+                                                                float2 *__restrict__ T1,
+                                                                const float2 *__restrict__ tw2, FusedWork w) {
+  constexpr int L = 2048, Q = L / 2 + 1, ROWS = 8, NP = ROWS / 2, RS = NP + 1, HALF = L / 4 + 1;
+  constexpr int PW = 1024, PWS = 1032, NT = 256;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float *ps = reinterpret_cast<float *>(smem_raw);    // [ROWS][PWS] new p rows
+  float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [2][HALF][RS] output staging (after the FFTs)
+  float2 *trb = reinterpret_cast<float2 *>(smem_raw); // [8][32][33] transposes
+  __shared__ double red[32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = warp >> 1, e = warp & 1;
+  const int b = blockIdx.y;
+  float be = 0.f, al = 0.f;
+  auto scalars = [&]() {
+    if (PLAIN) return;
+    const double rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
+    double beta = 0.0, alpha_prev = 0.0;
+    if (k > 0) {
+      const double rho_prev = w.rho[(size_t)b * w.rho_stride + k - 1];
+      beta = rho_prev > 0 ? rho / rho_prev : 0.0;
+      alpha_prev = w.alpha[b];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+      w.rho[(size_t)b * w.rho_stride + k] = rho;
+      if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
+    }
+    be = (float)beta;
+    al = (float)alpha_prev;
+  };
+  const int row0 = blockIdx.x * ROWS;
+  const int rows = min(ROWS, N - row0);
+  const size_t so = (size_t)b * N * N + (size_t)row0 * N;
+  constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
+  static_assert(ITEMS % (UB * NT) == 0, "every thread runs the same number of batches (the first one reduces)");
+  for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
+    float pv[UB][VW], rv[UB][VW], xv[UB][VW];
+    bool ok[UB];
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int i = i0 + u * NT;
+      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+      ok[u] = rr < rows && j < N;
+      if (ok[u]) {
+        const size_t e2 = so + (size_t)rr * N + j;
+        vload<float, VW>(pv[u], p + e2);
+        if (!PLAIN) {
+          vload<float, VW>(rv[u], r + e2);
+          vload<float, VW>(xv[u], x + e2);
+        }
+      }
+    }
+    if (i0 == (int)threadIdx.x) scalars();  // first batch: uniform across the CTA
+#pragma unroll
+    for (int u = 0; u < UB; ++u) {
+      const int i = i0 + u * NT;
+      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+      if (ok[u]) {
+        if (!PLAIN) {
+          const size_t e2 = so + (size_t)rr * N + j;
+#pragma unroll
+          for (int c = 0; c < VW; ++c) {
+            xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
+            pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+          }
+          vstore<float, VW>(x + e2, xv[u]);
+          vstore<float, VW>(p + e2, pv[u]);
+        }
+      } else {
+#pragma unroll
+        for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
+      }
+      vstore<float, VW>(ps + rr * PWS + j, pv[u]);
+    }
+  }
+  __syncthreads();
+  float2 v[32];
+#pragma unroll
+  for (int m = 0; m < 32; ++m) {
+    const float2 z{ps[(2 * pair) * PWS + lane + 32 * m], ps[(2 * pair + 1) * PWS + lane + 32 * m]};
+    v[m] = (e && m) ? cmul(z, __ldg(tw2 + 16 * 32 + m)) : z;  // z_r W_64^{r e}
+  }
+  __syncthreads();  // ps becomes the transpose buffers
+  dft32<false>(v);  // v[m] = Y[2m + e]
+  const float2 *twf = tw2 + e * 1024;
+#pragma unroll
+  for (int m = 0; m < 32; ++m)
+    if (e || m) v[m] = cmul(v[m], __ldg(twf + m * 32 + lane));  // W_2048^{(2m + e) t}
+  float2 *tr = trb + warp * (32 * 33);
+  warp_transpose32(v, tr, lane);  // lane m: v[t]
+  dft32<false>(v);                // v[kk] = Z[2 lane + e + 64 kk]
+  __syncthreads();  // transposes done CTA-wide: the area becomes the output staging tile
+  const int src = e ? 31 - lane : (32 - lane) & 31;
+  auto slot = [&](int q) { return st + ((q & 1) * HALF + (q >> 1)) * RS; };
+#pragma unroll
+  for (int kk = 0; kk <= 16; ++kk) {
+    float2 zc;
+    zc.x = __shfl_sync(0xffffffffu, v[(31 - kk) & 31].x, src);
+    zc.y = __shfl_sync(0xffffffffu, v[(31 - kk) & 31].y, src);
+    if (!e && lane == 0) zc = v[(32 - kk) & 31];
+    const int q = 2 * lane + e + 64 * kk;
+    if (kk < 16 || q == L / 2) {
+      const float2 z = v[kk];
+      slot(q)[pair] = make_float4(0.5f * (z.x + zc.x), 0.5f * (z.y - zc.y), 0.5f * (z.y + zc.y), 0.5f * (zc.x - z.x));
+    }
+  }
+  __syncthreads();
+  float2 *T1s = T1 + (size_t)b * Q * N + row0;
+  for (int i = threadIdx.x; i < Q * NP; i += blockDim.x) {
+    const int q = i / NP, pr = i % NP, rp = 2 * pr;
+    if (rp >= rows) continue;
+    const float4 c = slot(q)[pr];
+    float2 *dst = T1s + (size_t)q * N + rp;
+    if (rp + 1 < rows) {
+      if (!(N & 1)) {
+        *reinterpret_cast<float4 *>(dst) = c;
+      } else {
+        dst[0] = float2{c.x, c.y};
+        dst[1] = float2{c.z, c.w};
+      }
+    } else {
+      dst[0] = float2{c.x, c.y};
+    }
+  }
+}
+
 // ---------------------------------------------------------------- pass C: inverse row DFTs fused with the r update
 // MODE 0: CG (x deferred to pass A); 1: steepest descent; 2: Landweber (alpha = tau)
 template <typename T, int L, int MODE, int VW>
@@ -1107,6 +1243,24 @@ static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx
       return cudaGetLastError();
     }
   }
+  if constexpr (std::is_same<T, float>::value && L == 2048) {
+    if (pass_c_warp_enabled()) {
+      const float2 *tw2 = tw2048_table();
+      if (!tw2) return cudaErrorMemoryAllocation;
+      constexpr size_t sm = sizeof(float4) * 2 * (L / 4 + 1) * 5;
+      static_assert(sm >= sizeof(float) * 8 * 1032 && sm >= sizeof(float2) * 8 * 32 * 33, "pass A 2048 smem");
+      if (can_vec<T>(N, x, r, p)) {
+        cudaError_t e = cg_set_smem(cg_pass_a_2048_kernel<4, false>, sm);
+        if (e != cudaSuccess) return e;
+        cg_pass_a_2048_kernel<4, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, tw2, w);
+      } else {
+        cudaError_t e = cg_set_smem(cg_pass_a_2048_kernel<1, false>, sm);
+        if (e != cudaSuccess) return e;
+        cg_pass_a_2048_kernel<1, false><<<dim3(w.nparts, B), 256, sm, s>>>(N, k, x, r, p, T1, tw2, w);
+      }
+      return cudaGetLastError();
+    }
+  }
   if constexpr (std::is_same<T, float>::value && L == 512) {
     if (pass_c_warp_enabled()) {
       const float2 *twl = tw1024_table();
@@ -1236,7 +1390,26 @@ cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork
 // y = G x with the warp-FFT passes (FP32, L = 512 or 1024): pass A in PLAIN mode (x -> T1), pass B
 // (normal.cu), pass C in MODE 3 (T1 -> y).  Returns cudaErrorNotSupported otherwise.
 cudaError_t warp_apply_a(int N, int L, int B, const float *x, float2 *T1, cudaStream_t s) {
-  if ((L != 1024 && L != 512) || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  if ((L != 1024 && L != 512 && L != 2048) || !pass_c_warp_enabled()) return cudaErrorNotSupported;
+  if (L == 2048) {
+    const float2 *tw2 = tw2048_table();
+    if (!tw2) return cudaErrorMemoryAllocation;
+    constexpr size_t sm2 = sizeof(float4) * 2 * (2048 / 4 + 1) * 5;
+    FusedWork w{};
+    w.nparts = fused_parts(N, L, true);
+    w.B = B;
+    float *xp = const_cast<float *>(x);
+    if (can_vec<float>(N, x, nullptr, nullptr)) {
+      cudaError_t e = cg_set_smem(cg_pass_a_2048_kernel<4, true>, sm2);
+      if (e != cudaSuccess) return e;
+      cg_pass_a_2048_kernel<4, true><<<dim3(w.nparts, B), 256, sm2, s>>>(N, 0, nullptr, nullptr, xp, T1, tw2, w);
+    } else {
+      cudaError_t e = cg_set_smem(cg_pass_a_2048_kernel<1, true>, sm2);
+      if (e != cudaSuccess) return e;
+      cg_pass_a_2048_kernel<1, true><<<dim3(w.nparts, B), 256, sm2, s>>>(N, 0, nullptr, nullptr, xp, T1, tw2, w);
+    }
+    return cudaGetLastError();
+  }
   const float2 *twl = tw1024_table();
   if (!twl) return cudaErrorMemoryAllocation;
   if (L == 512) {

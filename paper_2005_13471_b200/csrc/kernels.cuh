@@ -67,7 +67,7 @@ template <typename T>
 cudaError_t pass_c(int N, int L, int B, const cplx<T> *T1, T *y, const cplx<T> *tw, cudaStream_t s);
 int pass_b_blocks(int L, bool fp32);  // CTAs per slice of pass B (gpart row length)
 bool pass_b_warp_enabled();           // FP32 L = 512 / 1024 / 2048 warp-level pass B (BSCT_PASSB_V1=1: off)
-bool pass_c_warp_enabled();           // FP32 L = 512 / 1024 warp-FFT passes A and C (BSCT_PASSC_V1=1: off)
+bool pass_c_warp_enabled();           // FP32 L = 512 / 1024 / 2048 warp-FFT passes A and C (BSCT_PASSC_V1=1: off)
 const float2 *tw1024_table();         // W_1024^{jt} [32][32] on the current device (lazily uploaded)
 const float2 *tw2048_table();         // W_2048^{(2m+e)t} [4][32][32] (pass B, L = 2048; lazily uploaded)
 bool bulk_stage_enabled();            // pass C T1 staging by bulk (TMA) copies (BSCT_BULK=1)

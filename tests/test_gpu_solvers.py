@@ -128,7 +128,7 @@ def test_reconstruct_host_matches_device(cuda_lib):
 @pytest.mark.parametrize("N", [129, 200, 256, 257, 300, 512, 700])
 @pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
 def test_warp_fft_passes_equal_generic(cuda_lib, N, solver, monkeypatch):
-    """FP32 warp-FFT passes (fft32.cuh; L = 512, 1024: passes A, B, C; L = 2048: passes B, C) against the
+    """FP32 warp-FFT passes (fft32.cuh; L = 512, 1024, 2048: passes A, B, C) against the
     generic block-FFT passes, ragged N (odd N exercises the unaligned staging path), B = 2."""
     cfg = CONFIGS[3].with_(N=N, n_angles=90, n_det=2 * N + 1, ellipse_scale=N / 64)
     T = gram_taps(cfg.geometry())
