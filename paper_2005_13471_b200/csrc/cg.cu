@@ -551,14 +551,11 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_2048_kernel(int N, int k, fl
 #pragma unroll
   for (int m = 0; m < 32; ++m) {
     const float2 z{ps[(2 * pair) * PWS + lane + 32 * m], ps[(2 * pair + 1) * PWS + lane + 32 * m]};
-    v[m] = (e && m) ? cmul(z, __ldg(tw2 + 16 * 32 + m)) : z;  // z_r W_64^{r e}
+    v[m] = e ? twiddle64<false>(z, m) : z;  // z_r W_64^{r e}
   }
   __syncthreads();  // ps becomes the transpose buffers
   dft32<false>(v);  // v[m] = Y[2m + e]
-  const float2 *twf = tw2 + e * 1024;
-#pragma unroll
-  for (int m = 0; m < 32; ++m)
-    if (e || m) v[m] = cmul(v[m], __ldg(twf + m * 32 + lane));  // W_2048^{(2m + e) t}
+twiddle2048_fwd(v, tw2, e, lane);  // W_2048^{(2m + e) t}
   float2 *tr = trb + warp * (32 * 33);
   warp_transpose32(v, tr, lane);  // lane m: v[t]
   dft32<false>(v);                // v[kk] = Z[2 lane + e + 64 kk]
@@ -1095,17 +1092,14 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_2048_kernel(int N, int k, in
     }
   }
   dft32<true>(v);  // over k: v[t] = U[2 lane + e][t]
-  const float2 *twi = tw2 + (2 + e) * 1024;
-#pragma unroll
-  for (int t = 0; t < 32; ++t)
-    if (e || t) v[t] = cmulc(v[t], __ldg(twi + t * 32 + lane));  // W_2048^{(2 lane + e) t}
+twiddle2048_inv(v, tw2, e, lane);  // conj W_2048^{(2 lane + e) t}
   __syncthreads();  // staging area becomes the transpose buffers
   float2 *tr = reinterpret_cast<float2 *>(smem_raw) + warp * (32 * 33);
   warp_transpose32(v, tr, lane);  // lane t: v[m] = U[2m + e][t]
   dft32<true>(v);                 // v[rr] = sum_m U[2m + e][t] W_32^{-rr m}
   if (e) {
 #pragma unroll
-    for (int rr = 1; rr < 32; ++rr) v[rr] = cmulc(v[rr], __ldg(tw2 + 16 * 32 + rr));  // W_64^{-rr}
+    for (int rr = 1; rr < 32; ++rr) v[rr] = twiddle64<true>(v[rr], rr);  // W_64^{-rr}
   }
 #pragma unroll
   for (int rr = 0; rr < 32; ++rr) tr[rr * 32 + lane] = v[rr];  // hand this half to the other warp

@@ -84,6 +84,72 @@ __device__ __forceinline__ void dft32(float2 *a) {
   for (int i = 0; i < 32; ++i) a[i] = o[i];
 }
 
+// cos(2 pi m / 64), compile-time (the W_64 factors of the L = 2048 parity split)
+__host__ __device__ constexpr double cos64(int m) {
+  m &= 63;
+  if (m > 32) m = 64 - m;  // even
+  const bool neg = m > 16;
+  if (neg) m = 32 - m;     // cos(pi - a) = -cos(a)
+  const double c = m == 0    ? 1.0
+         : m == 1  ? 0.99518472667219693
+         : m == 2  ? 0.98078528040323043
+         : m == 3  ? 0.95694033573220882
+         : m == 4  ? 0.92387953251128674
+         : m == 5  ? 0.88192126434835505
+         : m == 6  ? 0.83146961230254524
+         : m == 7  ? 0.77301045336273699
+         : m == 8  ? 0.70710678118654757
+         : m == 9  ? 0.63439328416364549
+         : m == 10 ? 0.55557023301960229
+         : m == 11 ? 0.47139673682599781
+         : m == 12 ? 0.38268343236508984
+         : m == 13 ? 0.29028467725446233
+         : m == 14 ? 0.19509032201612833
+         : m == 15 ? 0.09801714032956077
+                   : 0.0;
+  return neg ? -c : c;
+}
+__host__ __device__ constexpr double sin64(int m) { return cos64(m - 16); }
+
+// v * exp(-+ 2 pi i m / 64), m a compile-time constant after unrolling
+template <bool INV>
+__device__ __forceinline__ float2 twiddle64(float2 v, int m) {
+  m &= 63;
+  if (m == 0) return v;
+  const float c = (float)cos64(m);
+  const float s = INV ? (float)sin64(m) : -(float)sin64(m);
+  return crot(v, c, s);
+}
+
+// L = 2048 parity-split twiddles from tw2048_table() ([e][m][t] = W_2048^{(2m + e) t} and
+// [2 + e][t][m] the same): 8 + 3 table reads per 32 factors instead of 32 --
+// W^{(2m + e) t} = [e][4i][t] * W^{2 j t} for m = 4i + j (forward, lane t, register m) and
+// W^{(2m + e) t} = [2 + e][4i][m] * W^{(2m + e) j} for t = 4i + j (inverse, lane m, register t).
+__device__ __forceinline__ void twiddle2048_fwd(float2 *v, const float2 *__restrict__ tw2, int e, int lane) {
+  const float2 r1 = __ldg(tw2 + 1 * 32 + lane), r2 = __ldg(tw2 + 2 * 32 + lane), r3 = __ldg(tw2 + 3 * 32 + lane);
+  const float2 *T = tw2 + e * 1024;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 b = __ldg(T + (4 * i) * 32 + lane);
+    if (e || i) v[4 * i] = cmul(v[4 * i], b);
+    v[4 * i + 1] = cmul(cmul(v[4 * i + 1], b), r1);
+    v[4 * i + 2] = cmul(cmul(v[4 * i + 2], b), r2);
+    v[4 * i + 3] = cmul(cmul(v[4 * i + 3], b), r3);
+  }
+}
+__device__ __forceinline__ void twiddle2048_inv(float2 *v, const float2 *__restrict__ tw2, int e, int lane) {
+  const float2 *T = tw2 + (2 + e) * 1024;
+  const float2 s1 = __ldg(T + 1 * 32 + lane), s2 = __ldg(T + 2 * 32 + lane), s3 = __ldg(T + 3 * 32 + lane);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 b = __ldg(T + (4 * i) * 32 + lane);
+    if (e || i) v[4 * i] = cmulc(v[4 * i], b);
+    v[4 * i + 1] = cmulc(cmulc(v[4 * i + 1], b), s1);
+    v[4 * i + 2] = cmulc(cmulc(v[4 * i + 2], b), s2);
+    v[4 * i + 3] = cmulc(cmulc(v[4 * i + 3], b), s3);
+  }
+}
+
 // Warp transpose through shared memory: on entry lane l holds a[i] = M[l][i]; on exit lane l
 // holds a[i] = M[i][l].  tr: this warp's [32][33] float2 buffer.
 __device__ __forceinline__ void warp_transpose32(float2 *a, float2 *tr, int lane) {

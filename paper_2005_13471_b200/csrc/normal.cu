@@ -231,18 +231,15 @@ __global__ void __launch_bounds__(PB2_COLS * 64, 4) pass_b_2048_kernel(int N, fl
   float2 *col = T1 + ((size_t)b * Q + q) * N;
   float2 *tr = pb2_smem + warp * (32 * 33), *zx = pb2_smem + NWP * (32 * 33) + c * (32 * 32);
   const float *Sq = S + (size_t)q * L + 2 * lane + e;
-  const float2 *twf = tw2 + e * 1024, *twi = tw2 + (2 + e) * 1024;
   float2 v[32];
 #pragma unroll
   for (int r = 0; r < 32; ++r) {
     const int n = lane + 32 * r;
     const float2 xv = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
-    v[r] = (e && r) ? cmul(xv, __ldg(tw2 + 16 * 32 + r)) : xv;  // W_64^r = W_2048^{32 r}
+    v[r] = e ? twiddle64<false>(xv, r) : xv;  // x_r W_64^{r e}
   }
   dft32<false>(v);  // v[m] = Y[2m + e]
-#pragma unroll
-  for (int m = 0; m < 32; ++m)
-    if (e || m) v[m] = cmul(v[m], __ldg(twf + m * 32 + lane));  // W_2048^{(2m + e) t}
+twiddle2048_fwd(v, tw2, e, lane);  // W_2048^{(2m + e) t}
   warp_transpose32(v, tr, lane);  // lane m: v[t]
   dft32<false>(v);                // v[k] = X[2 lane + e + 64 k]
   float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};
@@ -253,14 +250,12 @@ __global__ void __launch_bounds__(PB2_COLS * 64, 4) pass_b_2048_kernel(int N, fl
     v[k] = w;
   }
   dft32<true>(v);  // over k: v[t] = U[2 lane + e][t]
-#pragma unroll
-  for (int t = 0; t < 32; ++t)
-    if (e || t) v[t] = cmulc(v[t], __ldg(twi + t * 32 + lane));  // W_2048^{(2 lane + e) t}
+twiddle2048_inv(v, tw2, e, lane);  // conj W_2048^{(2 lane + e) t}
   warp_transpose32(v, tr, lane);  // lane t: v[m] = U[2m + e][t]
   dft32<true>(v);                 // v[r] = sum_m U[2m + e][t] W_32^{-r m}
   if (e) {
 #pragma unroll
-    for (int r = 0; r < 32; ++r) zx[r * 32 + lane] = r ? cmulc(v[r], __ldg(tw2 + 16 * 32 + r)) : v[r];
+    for (int r = 0; r < 32; ++r) zx[r * 32 + lane] = twiddle64<true>(v[r], r);
   }
   __syncthreads();
   if (!e) {
