@@ -267,8 +267,7 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(in
   for (int m = 0; m < 16; ++m) v[m] = float2{ps[(2 * warp) * PW + lane + 32 * m], ps[(2 * warp + 1) * PW + lane + 32 * m]};
   __syncthreads();  // ps becomes the transpose buffers
   dft32<false, true>(v);  // over m (v[16..31] = 0): v[j] = sum_m z[lane + 32 m] W_32^{m j}
-#pragma unroll
-  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], __ldg(tw1024 + j * 32 + lane));
+  twiddle1024<false>(v, tw1024, lane);  // W_1024^{j t}
   float2 *tr = trb + warp * (32 * 33);
   warp_transpose32(v, tr, lane);  // lane j: v[t]
   dft32<false>(v);                // v[kk] = Z[lane + 32 kk]
@@ -817,8 +816,7 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_c_1024_kernel(in
   __syncthreads();  // staging area becomes the transpose buffers
   float2 *tr = reinterpret_cast<float2 *>(smem_raw) + warp * (32 * 33);
   dft32<true>(v);  // over rr: v[a] = U[lane][a]
-#pragma unroll
-  for (int a = 1; a < 32; ++a) v[a] = cmulc(v[a], __ldg(tw1024 + a * 32 + lane));
+  twiddle1024<true>(v, tw1024, lane);  // conj W_1024^{a t}
   warp_transpose32(v, tr, lane);  // lane a: v[j] = U[j][a]
   dft32<true>(v);                 // v[m] = z[lane + 32 m] = y_a + i y_b
   // streaming phase: r -= alpha (G d) (and x += alpha r for SD / Landweber)

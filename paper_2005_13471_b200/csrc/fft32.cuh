@@ -150,6 +150,28 @@ __device__ __forceinline__ void twiddle2048_inv(float2 *v, const float2 *__restr
   }
 }
 
+// v[j] *= W_1024^{j t} (INV: conj) for lane t, j = 1..31, from the [32][32] table with 8 + 3
+// reads instead of 31: W^{(4i + jj) t} = [4i][t] * [jj][t]
+template <bool INV>
+__device__ __forceinline__ void twiddle1024(float2 *v, const float2 *__restrict__ tw, int lane) {
+  const float2 r1 = __ldg(tw + 1 * 32 + lane), r2 = __ldg(tw + 2 * 32 + lane), r3 = __ldg(tw + 3 * 32 + lane);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 b = __ldg(tw + (4 * i) * 32 + lane);
+    if (INV) {
+      if (i) v[4 * i] = cmulc(v[4 * i], b);
+      v[4 * i + 1] = i ? cmulc(cmulc(v[4 * i + 1], b), r1) : cmulc(v[1], r1);
+      v[4 * i + 2] = i ? cmulc(cmulc(v[4 * i + 2], b), r2) : cmulc(v[2], r2);
+      v[4 * i + 3] = i ? cmulc(cmulc(v[4 * i + 3], b), r3) : cmulc(v[3], r3);
+    } else {
+      if (i) v[4 * i] = cmul(v[4 * i], b);
+      v[4 * i + 1] = i ? cmul(cmul(v[4 * i + 1], b), r1) : cmul(v[1], r1);
+      v[4 * i + 2] = i ? cmul(cmul(v[4 * i + 2], b), r2) : cmul(v[2], r2);
+      v[4 * i + 3] = i ? cmul(cmul(v[4 * i + 3], b), r3) : cmul(v[3], r3);
+    }
+  }
+}
+
 // Warp transpose through shared memory: on entry lane l holds a[i] = M[l][i]; on exit lane l
 // holds a[i] = M[i][l].  tr: this warp's [32][33] float2 buffer.
 __device__ __forceinline__ void warp_transpose32(float2 *a, float2 *tr, int lane) {
