@@ -125,7 +125,7 @@ def test_reconstruct_host_matches_device(cuda_lib):
     assert torch.equal(x.cpu(), xh)
 
 
-@pytest.mark.parametrize("N", [129, 200, 256, 257, 300, 512, 700])
+@pytest.mark.parametrize("N", [129, 200, 256, 257, 300, 512, 700, 701])
 @pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
 def test_warp_fft_passes_equal_generic(cuda_lib, N, solver, monkeypatch):
     """FP32 warp-FFT passes (fft32.cuh; L = 512, 1024, 2048: passes A, B, C) against the
