@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(FftLaunchB<L>::THREADS) pass_b_kernel(int N, c
 // first DFT_32 sees 16 literal zeros, and only the N <= 512 kept rows of the inverse are
 // formed.  No block-wide barrier; PB_WARPS columns per CTA share the W_1024 table.
 constexpr int PB_WARPS = 4;
+#ifndef BSCT_PB_CPW
+#define BSCT_PB_CPW 2  // measured: pass B 145 -> 139 ms per config-5 step (4: same as 2)
+#endif
+constexpr int PB_CPW = BSCT_PB_CPW;  // columns per warp (the W_1024 table fill is per CTA)
 
 // FULL: N == L / 2 (every load and store in range, no per-element guards; halves the code the
 // compiler emits, which otherwise versions the FFT body on the guards)
@@ -146,11 +150,12 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
   // warps past the last column recompute column Q - 1 and store nothing: no branch around the
   // FFT (its __syncwarp transposes in possibly-divergent code made the compiler emit a second,
   // divergent-path copy of the whole body)
-  const int q0 = blockIdx.x * PB_WARPS + warp;
-  const bool live = q0 < Q;
-  const int q = live ? q0 : Q - 1;
   double gam = 0.0;
-  {
+#pragma unroll 1
+  for (int cc = 0; cc < PB_CPW; ++cc) {
+    const int q0 = (blockIdx.x * PB_CPW + cc) * PB_WARPS + warp;
+    const bool live = q0 < Q;
+    const int q = live ? q0 : Q - 1;
     float2 *col = T1 + ((size_t)b * Q + q) * N;
     float2 v[32];
 #pragma unroll
@@ -175,9 +180,9 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
       g2[k & 1] = cfma2(w, v[k], g2[k & 1]);
       v[k] = w;
     }
-    gam = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
-    if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
-    if (!live) gam = 0.0;
+    double gc = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
+    if (q != 0 && q != L / 2) gc *= 2.0;  // the other half of the Hermitian spectrum
+    if (live) gam += gc;
     dft32<true>(v);  // over k: v[a] = U[lane][a]
 #pragma unroll
     for (int a = 1; a < 32; ++a) v[a] = cmulc(v[a], twl[a * 32 + lane]);
@@ -598,7 +603,7 @@ static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T>
     const float2 *twl = tw1024_table();
     if (!twl) return cudaErrorMemoryAllocation;
     if (pass_b_warp_enabled()) {
-      const dim3 grid((L / 2 + 1 + PB_WARPS - 1) / PB_WARPS, B);
+      const dim3 grid((L / 2 + 1 + PB_WARPS * PB_CPW - 1) / (PB_WARPS * PB_CPW), B);
       if (N == L / 2)
         pass_b_1024_kernel<true><<<grid, PB_WARPS * 32, 0, s>>>(N, T1, S, twl, gpart);
       else
@@ -671,7 +676,7 @@ bool pass_b_warp_enabled() {
 }
 
 int pass_b_blocks(int L, bool fp32) {
-  if (fp32 && L == 1024 && pass_b_warp_enabled()) return (1024 / 2 + 1 + PB_WARPS - 1) / PB_WARPS;  // FP32 warp kernel
+  if (fp32 && L == 1024 && pass_b_warp_enabled()) return (1024 / 2 + 1 + PB_WARPS * PB_CPW - 1) / (PB_WARPS * PB_CPW);
   if (fp32 && L == 512 && pass_b_warp_enabled()) return (512 / 2 + 1 + 2 * PB5_WARPS - 1) / (2 * PB5_WARPS);
   if (fp32 && L == 2048 && pass_b_warp_enabled()) return (2048 / 2 + 1 + PB2_COLS - 1) / PB2_COLS;
   switch (L) {
