@@ -298,6 +298,10 @@ twiddle2048_inv(v, tw2, e, lane);  // conj W_2048^{(2 lane + e) t}
 #define BSCT_PB5_MINB 4
 #endif
 constexpr int PB5_WARPS = BSCT_PB5_WARPS;
+#ifndef BSCT_PB5_CPW
+#define BSCT_PB5_CPW 2
+#endif
+constexpr int PB5_CPW = BSCT_PB5_CPW;
 
 template <bool FULL>
 __global__ void __launch_bounds__(PB5_WARPS * 32, BSCT_PB5_MINB) pass_b_512_kernel(int N, float2 *__restrict__ T1,
@@ -318,66 +322,70 @@ __global__ void __launch_bounds__(PB5_WARPS * 32, BSCT_PB5_MINB) pass_b_512_kern
   }
   __syncthreads();
   const int b = blockIdx.y;
-  const int q0 = (blockIdx.x * PB5_WARPS + warp) * 2 + h;
-  const bool live = q0 < Q;  // the last half-warps recompute column Q - 1 and store nothing
-  const int q = live ? q0 : Q - 1;
-  float2 *col = T1 + ((size_t)b * Q + q) * N;
-  float2 *tr = trs[warp][h];
-  float2 v[32];
+  double gam = 0.0;
+#pragma unroll 1
+  for (int cc = 0; cc < PB5_CPW; ++cc) {  // columns per half-warp (the table fill is per CTA)
+    const int q0 = ((blockIdx.x * PB5_CPW + cc) * PB5_WARPS + warp) * 2 + h;
+    const bool live = q0 < Q;  // the last half-warps recompute column Q - 1 and store nothing
+    const int q = live ? q0 : Q - 1;
+    float2 *col = T1 + ((size_t)b * Q + q) * N;
+    float2 *tr = trs[warp][h];
+    float2 v[32];
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int n = t + 16 * r;
-    v[r] = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
-  }
-  dft32<false, true>(v);  // v[j] = sum_r x[t + 16 r] W_32^{r j}
+    for (int r = 0; r < 16; ++r) {
+      const int n = t + 16 * r;
+      v[r] = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
+    }
+    dft32<false, true>(v);  // v[j] = sum_r x[t + 16 r] W_32^{r j}
 #pragma unroll
-  for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twl[j * 32 + t]);  // W_512^{t j} = entry (j, 2t)
+    for (int j = 1; j < 32; ++j) v[j] = cmul(v[j], twl[j * 32 + t]);  // W_512^{t j} = entry (j, 2t)
 #pragma unroll
-  for (int j = 0; j < 32; ++j) tr[j * 17 + t] = v[j];
-  __syncwarp();
-  float2 a0[16], a1[16];
+    for (int j = 0; j < 32; ++j) tr[j * 17 + t] = v[j];
+    __syncwarp();
+    float2 a0[16], a1[16];
 #pragma unroll
-  for (int tt = 0; tt < 16; ++tt) {
-    a0[tt] = tr[t * 17 + tt];
-    a1[tt] = tr[(t + 16) * 17 + tt];
-  }
-  __syncwarp();
-  dft_reg<16, false>(a0);  // a0[k] = X[t + 32 k]
-  dft_reg<16, false>(a1);  // a1[k] = X[t + 16 + 32 k]
-  const float *Sq = S + (size_t)q * L;
-  float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};  // packed Parseval partials, as in pass_b_1024_kernel
+    for (int tt = 0; tt < 16; ++tt) {
+      a0[tt] = tr[t * 17 + tt];
+      a1[tt] = tr[(t + 16) * 17 + tt];
+    }
+    __syncwarp();
+    dft_reg<16, false>(a0);  // a0[k] = X[t + 32 k]
+    dft_reg<16, false>(a1);  // a1[k] = X[t + 16 + 32 k]
+    const float *Sq = S + (size_t)q * L;
+    float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};  // packed Parseval partials, as in pass_b_1024_kernel
 #pragma unroll
-  for (int k = 0; k < 16; ++k) {
-    const float2 w0 = cscale(a0[k], Sq[t + 32 * k]), w1 = cscale(a1[k], Sq[t + 16 + 32 * k]);
-    g2[0] = cfma2(w0, a0[k], g2[0]);
-    g2[1] = cfma2(w1, a1[k], g2[1]);
-    a0[k] = w0;
-    a1[k] = w1;
-  }
-  double gam = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
-  if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
-  if (!live) gam = 0.0;
-  dft_reg<16, true>(a0);  // a0[tt] = U[j = t][tt]
-  dft_reg<16, true>(a1);  // a1[tt] = U[j = t + 16][tt]
+    for (int k = 0; k < 16; ++k) {
+      const float2 w0 = cscale(a0[k], Sq[t + 32 * k]), w1 = cscale(a1[k], Sq[t + 16 + 32 * k]);
+      g2[0] = cfma2(w0, a0[k], g2[0]);
+      g2[1] = cfma2(w1, a1[k], g2[1]);
+      a0[k] = w0;
+      a1[k] = w1;
+    }
+    double gc = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
+    if (q != 0 && q != L / 2) gc *= 2.0;  // the other half of the Hermitian spectrum
+    if (live) gam += gc;
+    dft_reg<16, true>(a0);  // a0[tt] = U[j = t][tt]
+    dft_reg<16, true>(a1);  // a1[tt] = U[j = t + 16][tt]
 #pragma unroll
-  for (int tt = 1; tt < 16; ++tt) {
-    a0[tt] = cmulc(a0[tt], twl[tt * 64 + (t >> 1) + 16 * (t & 1)]);       // entry (2 tt, t)
-    a1[tt] = cmulc(a1[tt], twl[tt * 64 + 8 + (t >> 1) + 16 * (t & 1)]);   // entry (2 tt, t + 16)
-  }
+    for (int tt = 1; tt < 16; ++tt) {
+      a0[tt] = cmulc(a0[tt], twl[tt * 64 + (t >> 1) + 16 * (t & 1)]);       // entry (2 tt, t)
+      a1[tt] = cmulc(a1[tt], twl[tt * 64 + 8 + (t >> 1) + 16 * (t & 1)]);   // entry (2 tt, t + 16)
+    }
 #pragma unroll
-  for (int tt = 0; tt < 16; ++tt) {
-    tr[t * 17 + tt] = a0[tt];
-    tr[(t + 16) * 17 + tt] = a1[tt];
-  }
-  __syncwarp();
+    for (int tt = 0; tt < 16; ++tt) {
+      tr[t * 17 + tt] = a0[tt];
+      tr[(t + 16) * 17 + tt] = a1[tt];
+    }
+    __syncwarp();
 #pragma unroll
-  for (int j = 0; j < 32; ++j) v[j] = tr[j * 17 + t];  // lane t: U[j][t]
-  __syncwarp();
-  dft32<true>(v);  // v[r] = z[t + 16 r]
+    for (int j = 0; j < 32; ++j) v[j] = tr[j * 17 + t];  // lane t: U[j][t]
+    __syncwarp();
+    dft32<true>(v);  // v[r] = z[t + 16 r]
 #pragma unroll
-  for (int r = 0; r < 16; ++r) {
-    const int n = t + 16 * r;
-    if (live && (FULL || n < N)) col[n] = v[r];
+    for (int r = 0; r < 16; ++r) {
+      const int n = t + 16 * r;
+      if (live && (FULL || n < N)) col[n] = v[r];
+    }
   }
   if (gpart) {  // deterministic CTA reduction
     for (int o = 16; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o);
@@ -631,7 +639,7 @@ static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T>
     const float2 *twl = tw1024_table();
     if (!twl) return cudaErrorMemoryAllocation;
     if (pass_b_warp_enabled()) {
-      const dim3 grid((L / 2 + 1 + 2 * PB5_WARPS - 1) / (2 * PB5_WARPS), B);
+      const dim3 grid((L / 2 + 1 + 2 * PB5_WARPS * PB5_CPW - 1) / (2 * PB5_WARPS * PB5_CPW), B);
       if (N == L / 2)
         pass_b_512_kernel<true><<<grid, PB5_WARPS * 32, 0, s>>>(N, T1, S, twl, gpart);
       else
@@ -677,7 +685,7 @@ bool pass_b_warp_enabled() {
 
 int pass_b_blocks(int L, bool fp32) {
   if (fp32 && L == 1024 && pass_b_warp_enabled()) return (1024 / 2 + 1 + PB_WARPS * PB_CPW - 1) / (PB_WARPS * PB_CPW);
-  if (fp32 && L == 512 && pass_b_warp_enabled()) return (512 / 2 + 1 + 2 * PB5_WARPS - 1) / (2 * PB5_WARPS);
+  if (fp32 && L == 512 && pass_b_warp_enabled()) return (512 / 2 + 1 + 2 * PB5_WARPS * PB5_CPW - 1) / (2 * PB5_WARPS * PB5_CPW);
   if (fp32 && L == 2048 && pass_b_warp_enabled()) return (2048 / 2 + 1 + PB2_COLS - 1) / PB2_COLS;
   switch (L) {
     case 2: return (2 / 2 + 1 + FftLaunchB<2>::G - 1) / FftLaunchB<2>::G;
