@@ -149,6 +149,22 @@ bsct_status bsct_cg_solve(bsct_plan plan, const void *b, void *x, int32_t B, int
                           double *resid_hist, int32_t *flags, bsct_stream stream);
 
 /*
+ * Resume (checkpoint / restart) of a solve on G x = b from a saved state after some iteration j
+ * (textbook recurrences, oracle/solvers.py):
+ *   x [B][N][N]  IN x_j, OUT x_{j+iters}
+ *   r [B][N][N]  IN r_j = b - G x_j, OUT r_{j+iters}
+ *   p [B][N][N]  (CG only; may be NULL for SD / Landweber) IN the search direction p_j,
+ *                OUT p_{j+iters} = r_{j+iters} + beta p_{j+iters-1}
+ * and runs `iters` iterations on the same fused kernels as bsct_cg_solve (the CG step from
+ * (x_j, r_j, p_j) is alpha = <r,r>/<p,Gp>, x += alpha p, r -= alpha G p, beta = <r',r'>/<r,r>).
+ * alpha_last: DEVICE double [B] receiving the step length of the last iteration, or NULL.
+ * resid_hist / flags as in bsct_cg_solve.  Used for R12 check (ii) (one step from the oracle's
+ * state) and to continue a solve in pieces.  All buffers caller-owned DEVICE memory.
+ */
+bsct_status bsct_cg_resume(bsct_plan plan, void *x, void *r, void *p, int32_t B, int32_t iters, int32_t solver,
+                           double *alpha_last, double *resid_hist, int32_t *flags, bsct_stream stream);
+
+/*
  * Forward projection g = H c (Eq.(3), Eq.(4)):
  *     g[t][m] = lambda_x^2 sum_k c_k M_[l|c|, l|s|, zeta](y_m - k_t)
  *     c [B][N][N] -> sino [B][n_angles][n_det].  (Support op: data synthesis, exactness checks.)

@@ -46,8 +46,8 @@ def cg(taps, b, iters: int, direct: bool = False, record=None):
         p = r + (rr_new / rr) * p
         rr = rr_new
         hist.append(np.sqrt(rr))
-        if record is not None:
-            record.append(dict(alpha=alpha, x=x.copy()))
+        if record is not None:  # state after this iteration (R12 check (ii) resumes from it)
+            record.append(dict(alpha=alpha, x=x.copy(), r=r.copy(), p=p.copy(), rr=rr))
     return x, np.array(hist)
 
 

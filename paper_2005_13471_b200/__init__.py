@@ -34,7 +34,7 @@ H_CORR = 25
 # exported symbols of include/bsct.h (checked by tests/test_abi.py)
 SYMBOLS = ("bsct_version", "bsct_last_error", "bsct_fft_size", "bsct_gram_build", "bsct_plan_create",
            "bsct_plan_destroy", "bsct_plan_set_filter", "bsct_plan_spectrum", "bsct_correction_filter", "bsct_backproject",
-           "bsct_normal_apply", "bsct_cg_solve", "bsct_forward_project", "bsct_reconstruct", "bsct_reconstruct_host",
+           "bsct_normal_apply", "bsct_cg_solve", "bsct_cg_resume", "bsct_forward_project", "bsct_reconstruct", "bsct_reconstruct_host",
            "bsct_adjoint_project", "bsct_sirt_solve", "bsct_chebyshev_solve",
            "bsct_plan_launch_count", "bsct_plan_profile", "bsct_plan_profile_read")
 
@@ -82,6 +82,7 @@ def load(path: str | None = None):
         "bsct_backproject": (i32, [vp, vp, vp, i32, vp]),
         "bsct_normal_apply": (i32, [vp, vp, vp, i32, vp]),
         "bsct_cg_solve": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
+        "bsct_cg_resume": (i32, [vp, vp, vp, vp, i32, i32, i32, vp, vp, vp, vp]),
         "bsct_forward_project": (i32, [vp, vp, vp, i32, vp]),
         "bsct_reconstruct": (i32, [vp, vp, vp, i32, i32, i32, vp, vp, vp]),
         "bsct_adjoint_project": (i32, [vp, vp, vp, i32, vp]),
@@ -268,6 +269,22 @@ def cg_solve(plan: Plan, b, x, iters: int, solver="cg", resid_hist=None, flags=N
                                 _ptr(resid_hist, torch.float64, B * iters, "resid_hist"),
                                 _ptr(flags, torch.int32, B, "flags"), _stream(stream)))
     return x
+
+
+def cg_resume(plan: Plan, x, r, p, iters: int, solver="cg", alpha_last=None, resid_hist=None, flags=None,
+              stream=None):
+    """Continue a solve from the state (x_j, r_j, p_j) for `iters` iterations; x, r, p are
+    updated in place to the final state (p: CG only, None for SD / Landweber)."""
+    import torch
+    B = _batch(x, plan.N * plan.N, "x")
+    sv = SOLVERS[solver] if isinstance(solver, str) else int(solver)
+    n = B * plan.N * plan.N
+    _check(load().bsct_cg_resume(plan.handle, _ptr(x, plan.dtype, n, "x"), _ptr(r, plan.dtype, n, "r"),
+                                 _ptr(p, plan.dtype, n, "p"), B, int(iters), sv,
+                                 _ptr(alpha_last, torch.float64, B, "alpha_last"),
+                                 _ptr(resid_hist, torch.float64, B * iters, "resid_hist"),
+                                 _ptr(flags, torch.int32, B, "flags"), _stream(stream)))
+    return x, r, p
 
 
 def reconstruct(plan: Plan, sino, x, iters: int, solver="cg", resid_hist=None, flags=None, stream=None):

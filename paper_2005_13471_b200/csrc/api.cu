@@ -179,6 +179,83 @@ void twiddles(int L, std::vector<double> &re, std::vector<double> &im) {
   }
 }
 
+// Library-owned stream-ordered memory pool of device `dev` (release threshold: keep everything),
+// so that the scratch of gram_build never touches the default pool other code in the process uses.
+cudaError_t lib_pool(int dev, cudaMemPool_t *out) {
+  static std::mutex mu;
+  static std::vector<std::pair<int, cudaMemPool_t>> pools;
+  std::lock_guard<std::mutex> lock(mu);
+  for (auto &e : pools)
+    if (e.first == dev) {
+      *out = e.second;
+      return cudaSuccess;
+    }
+  cudaMemPoolProps props = {};
+  props.allocType = cudaMemAllocationTypePinned;
+  props.location.type = cudaMemLocationTypeDevice;
+  props.location.id = dev;
+  cudaMemPool_t pool;
+  cudaError_t e = cudaMemPoolCreate(&pool, &props);
+  if (e != cudaSuccess) return e;
+  uint64_t thr = UINT64_MAX;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  if (e != cudaSuccess) return e;
+  pools.push_back({dev, pool});
+  *out = pool;
+  return cudaSuccess;
+}
+
+// Device copies of sorted angle sets (K1's input: angles sorted by t mod pi, then the bucket
+// table of gram.cu), cached per device by content so that repeated builds of the same geometry
+// enqueue no host->device copy and never wait on the stream.  Least recently used entries are
+// evicted beyond 64 per process; cudaFree of an evicted buffer waits for the device, so no
+// kernel still in flight can be reading it.
+constexpr int GRAM_NB = 4096;  // buckets of [0, pi)
+
+struct AngleSet {
+  int dev;
+  std::vector<double> key;
+  double *dptr;
+  uint64_t used;
+};
+
+cudaError_t gram_angles(int dev, const std::vector<double> &key, const std::vector<double> &sorted,
+                        const std::vector<int> &bucket, double **out) {
+  static std::mutex mu;
+  static std::vector<AngleSet> cache;
+  static uint64_t tick = 0;
+  std::lock_guard<std::mutex> lock(mu);
+  ++tick;
+  for (auto &e : cache)
+    if (e.dev == dev && e.key == key) {
+      e.used = tick;
+      *out = e.dptr;
+      return cudaSuccess;
+    }
+  if (cache.size() >= 64) {
+    auto lru = std::min_element(cache.begin(), cache.end(), [](auto &x, auto &y) { return x.used < y.used; });
+    int cur = 0;
+    cudaGetDevice(&cur);
+    cudaSetDevice(lru->dev);
+    cudaFree(lru->dptr);
+    cudaSetDevice(cur);
+    cache.erase(lru);
+  }
+  const size_t n = sorted.size();
+  double *d = nullptr;
+  cudaError_t e = cudaMalloc((void **)&d, sizeof(double) * n + sizeof(int) * bucket.size());
+  if (e != cudaSuccess) return e;
+  e = cudaMemcpy(d, sorted.data(), sizeof(double) * n, cudaMemcpyHostToDevice);
+  if (e == cudaSuccess) e = cudaMemcpy(d + n, bucket.data(), sizeof(int) * bucket.size(), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) {
+    cudaFree(d);
+    return e;
+  }
+  cache.push_back({dev, key, d, tick});
+  *out = d;
+  return cudaSuccess;
+}
+
 template <typename T>
 bsct_status gram_build_t(const bsct_geometry *g, int a0, int a1, T *taps, cudaStream_t s) {
   const int n = a1 - a0;
@@ -188,61 +265,43 @@ bsct_status gram_build_t(const bsct_geometry *g, int a0, int a1, T *taps, cudaSt
     CU(cudaMemsetAsync(taps, 0, D2 * sizeof(T), s));
     return BSCT_OK;
   }
-  static std::once_flag pool_once;
-  std::call_once(pool_once, [] {  // keep stream-ordered scratch in the pool between calls
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) == cudaSuccess && cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-      uint64_t thr = UINT64_MAX;
-      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-    }
-  });
+  int dev = 0;
+  CU(cudaGetDevice(&dev));
   const char *dense_env = getenv("BSCT_GRAM_DENSE");
   const bool dense = dense_env && dense_env[0] == '1';
-  // angles of the shard sorted by theta mod pi (window search of the windowed K1)
+  // angles of the shard sorted by t mod pi (K1's windows are runs of this order); the key is
+  // the shard's angles in the given order
   const double pi = 3.141592653589793238462643383279502884;
+  std::vector<double> key(g->angles + a0, g->angles + a1);
   std::vector<std::pair<double, double>> srt(n);
   for (int i = 0; i < n; ++i) {
-    const double t = g->angles[a0 + i];
-    srt[i] = {t - pi * std::floor(t / pi), t};
+    const double t = key[i];
+    double m = t - pi * std::floor(t / pi);
+    srt[i] = {std::min(std::max(m, 0.0), std::nextafter(pi, 0.0)), t};
   }
-  if (!dense) std::stable_sort(srt.begin(), srt.end(), [](auto &x, auto &y) { return x.first < y.first; });
-  std::vector<double> host(2 * (size_t)n);
-  for (int i = 0; i < n; ++i) {
-    host[i] = srt[i].second;
-    host[n + i] = std::min(std::max(srt[i].first, 0.0), std::nextafter(pi, 0.0));
+  std::stable_sort(srt.begin(), srt.end(), [](auto &x, auto &y) { return x.first < y.first; });
+  std::vector<double> sorted(n);
+  std::vector<int> bucket(GRAM_NB + 1);
+  for (int i = 0; i < n; ++i) sorted[i] = srt[i].second;
+  for (int k = 0, i = 0; k <= GRAM_NB; ++k) {  // bucket[k] = #{sorted: (t mod pi) < k pi / NB}
+    const double edge = k * (pi / GRAM_NB);
+    while (i < n && (k == GRAM_NB || srt[i].first < edge)) ++i;
+    bucket[k] = i;
   }
   double *ang = nullptr;
+  CU(gram_angles(dev, key, sorted, bucket, &ang));
+  const int *bk = (const int *)(ang + n);
+  cudaMemPool_t pool;
+  CU(lib_pool(dev, &pool));
   void *mem = nullptr;
-  bool ang_owned = false;
-  {
-    // device copies of angle sets are cached by content: repeated builds of the same
-    // geometry enqueue no host->device copy (and so never wait on the stream)
-    static std::mutex mu;
-    static std::vector<std::pair<std::pair<int, std::vector<double>>, double *>> cache;
-    std::lock_guard<std::mutex> lock(mu);
-    int dev = 0;
-    CU(cudaGetDevice(&dev));
-    for (auto &e : cache)
-      if (e.first.first == dev && e.first.second == host) ang = e.second;
-    if (!ang) {
-      CU(cudaMalloc((void **)&ang, sizeof(double) * 2 * n));
-      CU(cudaMemcpy(ang, host.data(), sizeof(double) * 2 * n, cudaMemcpyHostToDevice));
-      if (cache.size() < 256) cache.push_back({{dev, host}, ang});
-      else ang_owned = true;
-    }
-  }
-  CU(cudaMallocAsync(&mem, tables_bytes<T>(n), s));
+  const size_t tb_bytes = (tables_bytes<T>(n) + 255) & ~(size_t)255;
+  CU(cudaMallocFromPoolAsync(&mem, tb_bytes + sizeof(T) * (size_t)n * GR_WORDS, pool, s));
   PPTables<T> tb = tables_of<T>(mem, n);
+  tb.grec = (T *)((char *)mem + tb_bytes);
   CU(build_pp_tables<T>(ang, n, PP_GRAM, g->lambda_x, g->lambda_y, g->zeta_blur, tb, s));
-  if (dense) {
-    CU(gram_taps<T>(N, g->lambda_x, n, tb.cs, tb.view(), taps, s));
-  } else {
-    const double Hmax = (g->lambda_x * 1.4142135623730951 + g->zeta_blur) * (1.0 + 1e-12);
-    CU(gram_taps_window<T>(N, g->lambda_x, n, ang + n, tb.cs, tb.view(), Hmax, taps, s));
-  }
+  const double Hmax = (g->lambda_x * 1.4142135623730951 + g->zeta_blur) * (1.0 + 1e-12);
+  CU(gram_build_tiles<T>(N, g->lambda_x, n, tb.grec, bk, GRAM_NB, Hmax, dense, taps, s));
   CU(cudaFreeAsync(mem, s));
-  if (ang_owned) CU(cudaFreeAsync(ang, s));
   return BSCT_OK;
 }
 
@@ -276,7 +335,7 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   CU(cudaMemcpyAsync(p->tw, twh.data(), sizeof(cplx<T>) * twh.size(), cudaMemcpyHostToDevice, s));
   CU(cudaMalloc(&p->S, sizeof(T) * Q * L));
   CU(cudaMalloc(&p->spec_work, sizeof(cplx<T>) * Q * L));
-  CU(cudaMalloc((void **)&p->tau, sizeof(double)));
+  CU(cudaMalloc((void **)&p->tau, sizeof(double) * 256));  // [0] tau, [1..148] partial maxima
   const char *force_v1 = getenv("BSCT_BP_V1");
   p->bp_cells = (force_v1 && force_v1[0] == '1') ? 0 : bp_v2_max_cells(p->lx, p->ly, p->zeta);
   if (p->bp_cells > 0) {
@@ -518,6 +577,52 @@ bsct_status solve_launch_t(bsct_plan p, const T *b, T *x, int B, int iters, int 
     LAUNCH(p, BSCT_K_SOLVER_UPDATE, 1, (solver_update<T>(p->N, B, solver, it, iters, x, r, pp, q, w, s)));
     LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (solver_finish<T>(p->N, B, solver, it, iters, r, pp, w, s)));
   }
+  return BSCT_OK;
+}
+
+// Resume a solve from a saved state (x_j, r_j, p_j) for `iters` more iterations on the fused
+// passes (the same kernels as solve_launch_t), then export (r, p) of the final state in place.
+template <typename T>
+bsct_status resume_t(bsct_plan p, T *x, T *r_io, T *p_io, int B, int iters, int solver, double *alpha_out,
+                     double *resid, int *flags, cudaStream_t s) {
+  if (p->rho_iters < iters) {
+    if (p->rho) CU(cudaFree(p->rho));
+    p->rho = nullptr;
+    CU(cudaMalloc((void **)&p->rho, sizeof(double) * (size_t)(iters + 1) * (p->max_batch > 0 ? p->max_batch : 1)));
+    p->rho_iters = iters;
+    clear_graphs(p);
+  }
+  const bool cg = solver == BSCT_CG;
+  T *r = (T *)p->r, *pp = (T *)p->p, *q = (T *)p->q;
+  auto *T1 = (cplx<T> *)p->T1;
+  auto *tw = (const cplx<T> *)p->tw;
+  FusedWork fw;
+  fw.rho = p->rho;
+  fw.rho_stride = iters + 1;
+  fw.alpha = p->alpha;
+  fw.gpart = p->gpart;
+  fw.rpart = p->rpart;
+  fw.nparts = fused_parts(p->N, p->L, p->dt == BSCT_F32);
+  fw.B = B;
+  fw.flags = flags ? flags : p->flags;
+  fw.resid = resid;
+  fw.iters = iters;
+  fw.tau = p->tau;
+  const int gparts = pass_b_blocks(p->L, p->dt == BSCT_F32);
+  LAUNCH(p, BSCT_K_SOLVER_INIT, 1, (fused_resume<T>(p->N, B, r_io, cg ? p_io : (const T *)nullptr, r, cg ? pp : nullptr, q, fw, s)));
+  CU(cudaMemsetAsync(p->alpha, 0, sizeof(double) * B, s));
+  for (int it = 0; it < iters; ++it) {
+    if (cg)  // first resumed iteration: beta = alpha_prev = 0 and the "r" operand q = p_j, so p = p_j
+      LAUNCH(p, BSCT_K_PASS_A, 1, (fused_pass_a<T>(p->N, p->L, B, it, x, it == 0 ? q : r, pp, T1, tw, fw, s)));
+    else
+      LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, B, r, T1, tw, s)));
+    LAUNCH(p, BSCT_K_PASS_B, 1,
+           (pass_b<T>(p->N, p->L, B, T1, (const T *)p->S, tw, solver == BSCT_LANDWEBER ? nullptr : p->gpart, s)));
+    LAUNCH(p, BSCT_K_PASS_C, 1, (fused_pass_c<T>(p->N, p->L, B, it, solver, gparts, T1, x, r, tw, fw, s)));
+  }
+  LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, B, iters, cg, x, pp, fw, s)));
+  LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_export<T>(p->N, B, iters, r, pp, r_io, cg ? p_io : nullptr, fw, s)));
+  if (alpha_out) CU(cudaMemcpyAsync(alpha_out, p->alpha, sizeof(double) * B, cudaMemcpyDeviceToDevice, s));
   return BSCT_OK;
 }
 
@@ -863,6 +968,22 @@ bsct_status bsct_cg_solve(bsct_plan p, const void *b, void *x, int32_t B, int32_
   return p->dt == BSCT_F64
              ? solve_t<double>(p, (const double *)b, (double *)x, B, iters, solver, resid_hist, flags, s)
              : solve_t<float>(p, (const float *)b, (float *)x, B, iters, solver, resid_hist, flags, s);
+}
+
+bsct_status bsct_cg_resume(bsct_plan p, void *x, void *r, void *pdir, int32_t B, int32_t iters, int32_t solver,
+                           double *alpha_last, double *resid_hist, int32_t *flags, bsct_stream stream) {
+  bsct_status st = check_plan(p, B);
+  if (st != BSCT_OK) return st;
+  if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
+  if (solver < BSCT_CG || solver > BSCT_LANDWEBER) return fail(BSCT_EINVAL, "unknown solver %d", solver);
+  if (B == 0) return BSCT_OK;
+  if (!x || !r || (solver == BSCT_CG && !pdir)) return fail(BSCT_EINVAL, "NULL buffer");
+  p->launches = 0;
+  cudaStream_t s = (cudaStream_t)stream;
+  return p->dt == BSCT_F64 ? resume_t<double>(p, (double *)x, (double *)r, (double *)pdir, B, iters, solver,
+                                              alpha_last, resid_hist, flags, s)
+                           : resume_t<float>(p, (float *)x, (float *)r, (float *)pdir, B, iters, solver, alpha_last,
+                                             resid_hist, flags, s);
 }
 
 bsct_status bsct_forward_project(bsct_plan p, const void *c, void *sino, int32_t B, bsct_stream stream) {

@@ -11,6 +11,8 @@
 //     inside C_t's support contribute.
 #include <algorithm>
 #include <cmath>
+#include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "pptable.cuh"
@@ -26,10 +28,17 @@ template <typename T> __device__ __forceinline__ T qtap(int i);
 template <> __device__ __forceinline__ float qtap<float>(int i) { return c_q32[i]; }
 template <> __device__ __forceinline__ double qtap<double>(int i) { return c_q64[i]; }
 
-static bool g_q_ready = false;
-
+// q lives in __constant__ memory, which exists per device: uploaded once per device (the
+// flags are per device and guarded by a mutex, so a second GPU of the same process gets its
+// own copy instead of convolving with q = 0).
 static cudaError_t upload_q() {
-  if (g_q_ready) return cudaSuccess;
+  static std::mutex mu;
+  static std::vector<int> ready;  // devices whose c_q32 / c_q64 hold q
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  if (std::find(ready.begin(), ready.end(), dev) != ready.end()) return cudaSuccess;
   double q[2 * HC + 1];
   float qf[2 * HC + 1];
   const long double z = 2.0L * sqrtl(2.0L) - 3.0L;
@@ -39,9 +48,9 @@ static cudaError_t upload_q() {
     q[m + HC] = (double)v;
     qf[m + HC] = (float)v;
   }
-  cudaError_t e = cudaMemcpyToSymbol(c_q64, q, sizeof(q));
+  e = cudaMemcpyToSymbol(c_q64, q, sizeof(q));
   if (e == cudaSuccess) e = cudaMemcpyToSymbol(c_q32, qf, sizeof(qf));
-  if (e == cudaSuccess) g_q_ready = true;
+  if (e == cudaSuccess) ready.push_back(dev);
   return e;
 }
 

@@ -63,6 +63,53 @@ __global__ void __launch_bounds__(256) cg_init_kernel(long n, const T *__restric
   if (blockIdx.x == 0 && threadIdx.x == 0 && w.flags) w.flags[blockIdx.y] = 0;
 }
 
+// ---------------------------------------------------------------- resume: a saved CG/SD/LW state (x_j, r_j, p_j)
+// r = r_in, p = q = p_in (q feeds pass A's "r" operand at the first resumed iteration, where
+// beta = alpha_prev = 0, so pass A leaves x unchanged and forms p = q + 0 p = p_in exactly);
+// partials of <r_j, r_j> (parity 0).  x is the caller's buffer, updated in place.
+template <typename T>
+__global__ void __launch_bounds__(256) cg_resume_kernel(long n, const T *__restrict__ r_in,
+                                                        const T *__restrict__ p_in, T *__restrict__ r,
+                                                        T *__restrict__ p, T *__restrict__ q, FusedWork w) {
+  __shared__ double red[32];
+  const size_t off = (size_t)blockIdx.y * n;
+  double acc = 0;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const T v = r_in[off + i];
+    r[off + i] = v;
+    if (p) {
+      const T u = p_in[off + i];
+      p[off + i] = u;
+      q[off + i] = u;
+    }
+    acc += (double)v * v;
+  }
+  const double s = cta_sum(acc, red);
+  if (threadIdx.x == 0) w.rpart[(size_t)blockIdx.y * w.nparts + blockIdx.x] = s;  // parity 0
+  if (blockIdx.x == 0 && threadIdx.x == 0 && w.flags) w.flags[blockIdx.y] = 0;
+}
+
+// export the state after iteration K for a later resume: r_out = r_K and (CG)
+// p_out = r_K + beta_K p_{K-1}, beta_K = rho_K / rho_{K-1} -- the same fma as pass A's p update
+template <typename T>
+__global__ void __launch_bounds__(256) cg_export_kernel(long n, int K, const T *__restrict__ r,
+                                                        const T *__restrict__ p, T *__restrict__ r_out,
+                                                        T *__restrict__ p_out, FusedWork w) {
+  const int b = blockIdx.y;
+  double beta = 0.0;
+  if (p_out && K > 0) {
+    const double rho = w.rho[(size_t)b * w.rho_stride + K], rho_prev = w.rho[(size_t)b * w.rho_stride + K - 1];
+    beta = rho_prev > 0 ? rho / rho_prev : 0.0;
+  }
+  const T be = (T)beta;
+  const size_t off = (size_t)b * n;
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const T rv = r[off + i];
+    r_out[off + i] = rv;
+    if (p_out) p_out[off + i] = (K > 0) ? fma(be, p[off + i], rv) : p[off + i];
+  }
+}
+
 // VW-wide (16-byte when VW = 16/sizeof(T)) global loads / stores
 template <typename T, int VW>
 __device__ __forceinline__ void vload(T *dst, const T *__restrict__ src) {
@@ -1361,6 +1408,20 @@ cudaError_t fused_init(int N, int B, const T *b, T *x, T *r, T *p, FusedWork w, 
   return cudaGetLastError();
 }
 template <typename T>
+cudaError_t fused_resume(int N, int B, const T *r_in, const T *p_in, T *r, T *p, T *q, FusedWork w, cudaStream_t s) {
+  cg_resume_kernel<T><<<dim3(w.nparts, B), 256, 0, s>>>((long)N * N, r_in, p_in, r, p, q, w);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t fused_export(int N, int B, int K, const T *r, const T *p, T *r_out, T *p_out, FusedWork w,
+                         cudaStream_t s) {
+  const long n = (long)N * N;
+  int vb = (int)((n + 2047) / 2048);
+  vb = vb < 1 ? 1 : (vb > 128 ? 128 : vb);
+  cg_export_kernel<T><<<dim3(vb, B), 256, 0, s>>>(n, K, r, p, r_out, p_out, w);
+  return cudaGetLastError();
+}
+template <typename T>
 cudaError_t fused_pass_a(int N, int L, int B, int k, T *x, const T *r, T *p, cplx<T> *T1, const cplx<T> *tw,
                          FusedWork w, cudaStream_t s) {
   CG_L_SWITCH(L, return (cg_pass_a_L<T, LL>(N, B, k, x, r, p, T1, tw, w, s)));
@@ -1480,7 +1541,9 @@ cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaSt
                                        FusedWork, cudaStream_t);                                               \
   template cudaError_t fused_pass_c<T>(int, int, int, int, int, int, const cplx<T> *, T *, T *, const cplx<T> *, \
                                        FusedWork, cudaStream_t);                                               \
-  template cudaError_t fused_final<T>(int, int, int, int, T *, const T *, FusedWork, cudaStream_t);
+  template cudaError_t fused_final<T>(int, int, int, int, T *, const T *, FusedWork, cudaStream_t);             \
+  template cudaError_t fused_resume<T>(int, int, const T *, const T *, T *, T *, T *, FusedWork, cudaStream_t); \
+  template cudaError_t fused_export<T>(int, int, int, const T *, const T *, T *, T *, FusedWork, cudaStream_t);
 CG_INST(float)
 CG_INST(double)
 

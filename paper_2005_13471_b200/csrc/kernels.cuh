@@ -8,6 +8,14 @@
 
 namespace bsct {
 
+// Gram record of one angle (K0 -> K1), GR_WORDS elements of the table type T:
+//   [0] C_hi [1] C_lo [2] S_hi [3] S_lo   lambda_x cos t, lambda_x sin t (FP32: hi/lo split, gram.cu;
+//                                         FP64: hi = value, lo = 0)
+//   [GR_H] H = W/2                        half support
+//   [GR_KN .. +16) knots of the right half, knot 0 = 0, +inf beyond the last piece
+//   [GR_CO .. +16*GR_NC) local Taylor coefficients of each piece (degree <= 5)
+constexpr int GR_H = 4, GR_KN = 8, GR_MAXP = 16, GR_NC = 6, GR_CO = GR_KN + GR_MAXP, GR_WORDS = GR_CO + GR_MAXP * GR_NC;
+
 // Mutable device storage of per-angle tables (tables.cu).
 template <typename T>
 struct PPTables {
@@ -18,6 +26,7 @@ struct PPTables {
   double *knots = nullptr;  // [n][PP_MAXP+1]
   T *coef = nullptr;        // [n][PP_MAXP][PP_NC]
   double *cs = nullptr;     // [n][2]  cos t, sin t
+  T *grec = nullptr;        // [n][GR_WORDS] Gram records (PP_GRAM only; not carved, set by the caller)
   PPView<T> view() const { return PPView<T>{npieces, nwidths, half, knots, coef}; }
   static size_t bytes(int n) {
     return (size_t)n * (3 * sizeof(int) + sizeof(double) * (1 + (PP_MAXP + 1) + 2) + sizeof(T) * PP_MAXP * PP_NC) +
@@ -42,13 +51,13 @@ template <typename T>
 cudaError_t build_pp_tables(const double *angles_dev, int n, int kind, double lx, double ly, double zeta,
                             PPTables<T> out, cudaStream_t s);
 
-// K1 (gram.cu): taps[(2N-1)^2] = lx^4 sum_{a < n} M_a(lx <(-s_a, c_a), dk>)
+// K1 (gram.cu): taps[(2N-1)^2] = lx^4 sum_{a < n} M_a(lx <(-s_a, c_a), dk>) from the per-angle
+// Gram records (GramRec layout, written by K0 when PPTables::grec is set) of angles sorted by
+// t mod pi; bucket[k] (k = 0..nb) = number of sorted angles with (t mod pi) < k pi / nb;
+// Hmax >= max_t W_t / 2.  dense: every (tap, angle) pair (measurement mode).
 template <typename T>
-cudaError_t gram_taps(int N, double lx, int n, const double *cs, PPView<T> tb, T *taps, cudaStream_t s);
-// windowed K1: angles sorted mod pi (theta_sorted ascending in [0, pi)); Hmax >= max_t W_t/2
-template <typename T>
-cudaError_t gram_taps_window(int N, double lx, int n, const double *theta_sorted, const double *cs, PPView<T> tb,
-                             double Hmax, T *taps, cudaStream_t s);
+cudaError_t gram_build_tiles(int N, double lx, int n, const T *rec, const int *bucket, int nb, double Hmax, bool dense,
+                             T *taps, cudaStream_t s);
 
 // K2 (normal.cu): S[q][p] = Re DFT2(E)[p][q] / L^2, work >= (L/2+1)*L complex
 template <typename T>
@@ -174,6 +183,13 @@ cudaError_t fused_pass_c(int N, int L, int B, int k, int mode, int gparts, const
                          const cplx<T> *tw, FusedWork w, cudaStream_t s);
 template <typename T>
 cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork w, cudaStream_t s);
+// resume from a saved state (x_j, r_j, p_j): r = r_in, p = q = p_in, partials of <r_j, r_j>
+template <typename T>
+cudaError_t fused_resume(int N, int B, const T *r_in, const T *p_in, T *r, T *p, T *q, FusedWork w, cudaStream_t s);
+// export r_K and (p_out != null) p_K = r_K + beta_K p_{K-1}
+template <typename T>
+cudaError_t fused_export(int N, int B, int K, const T *r, const T *p, T *r_out, T *p_out, FusedWork w,
+                         cudaStream_t s);
 template <typename T>
 cudaError_t solver_init(int N, int B, const T *b, T *x, T *r, T *p, SolverWork w, int iters, cudaStream_t s);
 template <typename T>

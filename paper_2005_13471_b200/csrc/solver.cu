@@ -144,31 +144,37 @@ cudaError_t solver_finish(int N, int B, int solver, int it, int iters, const T *
   return cudaGetLastError();
 }
 
+constexpr int SPEC_MAX_CTAS = 148;  // one CTA per SM; out[1 .. SPEC_MAX_CTAS] hold the partial maxima
+
 template <typename T>
 __global__ void __launch_bounds__(VT) spectrum_max_kernel(long n, const T *__restrict__ S, double *out) {
   __shared__ double red[32];
   double m = -1e300;
-  for (long i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, (double)S[i]);
+  for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
+    m = fmax(m, (double)S[i]);
   for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
   __syncthreads();
   if (threadIdx.x == 0) {
     double mm = red[0];
     for (int i = 1; i < (int)(blockDim.x >> 5); ++i) mm = fmax(mm, red[i]);
-    *out = mm;
+    out[1 + blockIdx.x] = mm;
   }
 }
 
-// out = 1 / (L^2 max S) = 1 / max(DFT of the embedding): the Landweber step
-template <typename T>
-__global__ void tau_kernel(int L, double *m) {
-  *m = 1.0 / ((double)L * (double)L * *m);
+// out[0] = 1 / (L^2 max S) = 1 / max(DFT of the embedding): the Landweber step (max of the
+// partial maxima: exact, so independent of the partition)
+__global__ void __launch_bounds__(32) tau_kernel(int L, int parts, double *out) {
+  double m = -1e300;
+  for (int i = threadIdx.x; i < parts; i += 32) m = fmax(m, out[1 + i]);
+  for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if (threadIdx.x == 0) out[0] = 1.0 / ((double)L * (double)L * m);
 }
 
 template <typename T>
 cudaError_t spectrum_max(int L, const T *S, double *out, cudaStream_t s) {
-  spectrum_max_kernel<T><<<1, VT, 0, s>>>((long)(L / 2 + 1) * L, S, out);
-  tau_kernel<T><<<1, 1, 0, s>>>(L, out);
+  spectrum_max_kernel<T><<<SPEC_MAX_CTAS, VT, 0, s>>>((long)(L / 2 + 1) * L, S, out);
+  tau_kernel<<<1, 32, 0, s>>>(L, SPEC_MAX_CTAS, out);
   return cudaGetLastError();
 }
 

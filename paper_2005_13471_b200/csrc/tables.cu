@@ -13,14 +13,9 @@
 
 namespace bsct {
 
-__device__ __forceinline__ double ipow(double x, int e) {
-  double r = 1.0;
-  for (int i = 0; i < e; ++i) r *= x;
-  return r;
-}
 
 template <typename T>
-__global__ void __launch_bounds__(64) build_pp_tables_kernel(const double *__restrict__ angles, int n, int kind,
+__global__ void __launch_bounds__(128) build_pp_tables_kernel(const double *__restrict__ angles, int n, int kind,
                                                              double lx, double ly, double zeta, PPTables<T> out) {
   const int a = blockIdx.x;
   const int tid = threadIdx.x;
@@ -31,12 +26,18 @@ __global__ void __launch_bounds__(64) build_pp_tables_kernel(const double *__res
   __shared__ double sorted[64];
   __shared__ double kn[PP_MAXP + 1];
   __shared__ int K;
+  __shared__ double csh[2];
+  __shared__ unsigned kmask[2];
+  // let a programmatic dependent (K1 of gram_build) launch now: its prologue does not read the tables
+  asm volatile("griddepcontrol.launch_dependents;");
   if (a >= n) return;
   if (tid == 0) {
     double s, c;
     sincos(angles[a], &s, &c);
     out.cs[2 * a] = c;
     out.cs[2 * a + 1] = s;
+    csh[0] = c;
+    csh[1] = s;
     const double ac = lx * fabs(c), as = lx * fabs(s);
     double raw[8];
     int nr = 0;
@@ -90,30 +91,101 @@ __global__ void __launch_bounds__(64) build_pp_tables_kernel(const double *__res
   for (int i = 0; i < n_w; ++i) W += w[i];
   const double H = 0.5 * W;
   const double tol = 1e-12 * fmax(1.0, W);
-  if (tid == 0) {
-    int KK = 0;
-    kn[0] = 0.0;
-    for (int i = 0; i < ns; ++i) {
-      const double x = sorted[i] - H;
-      if (x > kn[KK] + tol && KK < PP_MAXP) kn[++KK] = x;
+  // Knots of the right half: the sorted subset sums minus H, a new knot wherever a value exceeds
+  // its predecessor (or 0) by more than tol (clusters of equal sums within tol merge into their
+  // first member); each flagged value's knot index is the prefix count of the flags.
+  {
+    const int lane = tid & 31, wp = tid >> 5;
+    bool flag = false;
+    double x = 0.0;
+    if (tid < ns) {
+      x = sorted[tid] - H;
+      const double prev = tid > 0 ? fmax(sorted[tid - 1] - H, 0.0) : 0.0;
+      flag = x > prev + tol;
     }
-    kn[KK] = H;  // the full-set sum closes the support
-    K = KK;
-    out.npieces[a] = KK;
-    out.half[a] = H;
+    const unsigned m = __ballot_sync(0xffffffffu, flag);
+    if (lane == 0 && wp < 2) kmask[wp] = m;
+    __syncthreads();
+    if (flag) {
+      const int idx = 1 + __popc(m & ((1u << lane) - 1u)) + (wp == 1 ? __popc(kmask[0]) : 0);
+      if (idx <= PP_MAXP) kn[idx] = x;
+    }
+    if (tid == 0) {
+      int KK = __popc(kmask[0]) + __popc(kmask[1]);
+      KK = KK < PP_MAXP ? KK : PP_MAXP;
+      kn[0] = 0.0;
+      K = KK;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      kn[K] = H;  // the full-set sum closes the support
+      out.npieces[a] = K;
+      out.half[a] = H;
+    }
+    __syncthreads();
   }
-  __syncthreads();
   for (int i = tid; i <= PP_MAXP; i += blockDim.x) out.knots[(size_t)a * (PP_MAXP + 1) + i] = i <= K ? kn[i] : H;
+  T *rg = (kind == PP_GRAM && out.grec) ? out.grec + (size_t)a * GR_WORDS : nullptr;
+  if (rg && tid < GR_MAXP) rg[GR_KN + tid] = tid <= K ? (T)kn[tid] : (T)INFINITY;
+  if (rg && tid == 0) {  // argument coefficients (gram.cu header: hi/lo split for FP32) and H
+    const double C = lx * csh[0], S = lx * csh[1];
+    if (sizeof(T) == 4) {
+      int e;
+      frexp(lx, &e);                         // lx <= 2^e
+      const double q0 = ldexp(1.0, e - 11);  // |hi| / q0 <= 2^11
+      const double ch = rint(C / q0) * q0, sh = rint(S / q0) * q0;
+      rg[0] = (T)ch;
+      rg[1] = (T)(C - ch);
+      rg[2] = (T)sh;
+      rg[3] = (T)(S - sh);
+    } else {
+      rg[0] = (T)C;
+      rg[1] = (T)0;
+      rg[2] = (T)S;
+      rg[3] = (T)0;
+    }
+    rg[GR_H] = (T)H;
+    rg[5] = rg[6] = rg[7] = (T)0;
+  }
   double prodw = 1.0;
   for (int i = 0; i < n_w; ++i) prodw *= w[i];
   double fact = 1.0;
   for (int i = 2; i < n_w; ++i) fact *= i;
   const double norm = 1.0 / (fact * prodw);
   const int deg = n_w - 1;
-  for (int j = tid; j < PP_MAXP; j += blockDim.x) {
+  // Local Taylor coefficients: 4 threads per piece, each summing every 4th subset; the four
+  // partial sums are combined by a fixed xor-shuffle tree.
+  const int part = tid & 3;
+  for (int jb = 0; jb < PP_MAXP; jb += (int)blockDim.x / 4) {
+    const int j = jb + tid / 4;
+    // ae[e] = sum over active subsets of sgn dl^e (powers as left-to-right products 1 * dl * dl ...)
+    double ae[PP_MAXW] = {0, 0, 0, 0, 0, 0};
+    if (j < K && n_w > 1) {
+      const double u0 = kn[j] + H;
+      for (int S = part; S < ns; S += 4) {
+        if (sig[S] > u0 + tol) continue;  // inactive on this piece
+        const double dl = fmax(0.0, u0 - sig[S]);
+        const double sg = (double)sgn[S];
+        double pw = 1.0;
+#pragma unroll
+        for (int e = 0; e < PP_MAXW; ++e) {
+          ae[e] += sg * pw;
+          pw *= dl;
+        }
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < PP_MAXW; ++e) {
+      ae[e] += __shfl_xor_sync(0xffffffffu, ae[e], 1);
+      ae[e] += __shfl_xor_sync(0xffffffffu, ae[e], 2);
+    }
+    if (part != 0 || j >= PP_MAXP) continue;
     T *cj = out.coef + ((size_t)a * PP_MAXP + j) * PP_NC;
+    T *gj = (rg && j < GR_MAXP) ? rg + GR_CO + j * GR_NC : nullptr;
     if (j >= K) {
       for (int k = 0; k < PP_NC; ++k) cj[k] = (T)0;
+      if (gj)
+        for (int k = 0; k < GR_NC; ++k) gj[k] = (T)0;
       continue;
     }
     if (n_w == 1) {  // plain box: constant 1/w (evaluated half-open in pptable.cuh)
@@ -121,21 +193,22 @@ __global__ void __launch_bounds__(64) build_pp_tables_kernel(const double *__res
       for (int k = 1; k < PP_NC; ++k) cj[k] = (T)0;
       continue;
     }
-    const double u0 = kn[j] + H;
-    double acc[PP_MAXW] = {0, 0, 0, 0, 0, 0};
-    for (int S = 0; S < ns; ++S) {
-      if (sig[S] > u0 + tol) continue;  // inactive on this piece
-      const double dl = fmax(0.0, u0 - sig[S]);
-      for (int k = 0; k <= deg; ++k) acc[k] += sgn[S] * ipow(dl, deg - k);
-    }
-    double binom = 1.0;  // C(deg, k)
-    for (int k = 0; k < PP_NC; ++k) {
-      if (k <= deg) {
-        cj[k] = (T)(norm * binom * acc[k]);
-        binom = binom * (deg - k) / (k + 1);
-      } else {
-        cj[k] = (T)0;
+    // coefficient of t^k, k = deg - e: norm C(deg, k) ae[e] with C(deg, k) = C(deg, e) (exact integer
+    // recursion over e, compile-time divisors after unrolling); ae stays in registers
+    int binom = 1;
+#pragma unroll
+    for (int e = 0; e < PP_MAXW; ++e) {
+      if (e <= deg) {
+        const int k = deg - e;
+        const T v = (T)(norm * (double)binom * ae[e]);
+        cj[k] = v;
+        if (gj && k < GR_NC) gj[k] = v;
+        binom = binom * (deg - e) / (e + 1);
       }
+    }
+    for (int k = deg + 1; k < PP_NC; ++k) {
+      cj[k] = (T)0;
+      if (gj && k < GR_NC) gj[k] = (T)0;
     }
   }
 }
@@ -144,7 +217,7 @@ template <typename T>
 cudaError_t build_pp_tables(const double *angles_dev, int n, int kind, double lx, double ly, double zeta,
                             PPTables<T> out, cudaStream_t s) {
   if (n <= 0) return cudaSuccess;
-  build_pp_tables_kernel<T><<<n, 64, 0, s>>>(angles_dev, n, kind, lx, ly, zeta, out);
+  build_pp_tables_kernel<T><<<n, 128, 0, s>>>(angles_dev, n, kind, lx, ly, zeta, out);
   return cudaGetLastError();
 }
 

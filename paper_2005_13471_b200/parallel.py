@@ -47,7 +47,17 @@ def gram_build_sharded(geom: dict, taps, group=None, stream=None):
     rank = dist.get_rank(group)
     a0, a1 = angle_shard(len(geom["angles"]), world, rank)
     gram_build(geom, taps, a0, a1, stream=stream)
+    _order_before_collective(stream)
     return allreduce_taps(taps, group)
+
+
+def _order_before_collective(stream):
+    """torch's NCCL collectives are ordered after work on torch's CURRENT stream only: when the
+    library call ran on another stream, make the current stream wait for it (no host sync)."""
+    if stream is None:
+        return
+    import torch
+    torch.cuda.current_stream().wait_stream(stream)
 
 
 def angle_shard_geometry(geom: dict, world: int, rank: int) -> tuple[dict, int, int]:
@@ -70,7 +80,6 @@ def backproject_sharded(plan_shard, sino_shard, b, group=None, stream=None):
         b.zero_()
     else:
         backproject(plan_shard, sino_shard, b, stream=stream)
-    if stream is not None:
-        stream.synchronize()
+    _order_before_collective(stream)
     dist.all_reduce(b, op=dist.ReduceOp.SUM, group=group)
     return b

@@ -82,3 +82,31 @@ def test_angle_shards_sum(cuda_lib):
     assert rel_l2(to_np(parts), to_np(full)) < 1e-6
     cuda_lib.gram_build(g, tmp, 5, 5)                # empty shard -> zeros
     assert not tmp.any()
+
+
+def test_gram_build_sharded_nccl(cuda_lib):
+    """parallel.gram_build_sharded end to end on a one-rank NCCL group, the build queued on a
+    non-current stream (the allreduce must be ordered after it), against the oracle; the
+    angle-shard arithmetic over 4 ranks is covered by tests/test_parallel_gloo.py."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2005_13471_b200.parallel import gram_build_sharded
+    g = geom(96, uniform(120), 193, zeta=0.5, lambda_y=0.5)
+    ref = gram_taps(g)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1)
+    try:
+        side = torch.cuda.Stream()
+        for _ in range(3):
+            taps = torch.full((191, 191), float("nan"), device="cuda")
+            gram_build_sharded(g, taps, stream=side)
+            torch.cuda.synchronize()
+            assert rel_l2(to_np(taps), ref) < 1e-5
+    finally:
+        dist.destroy_process_group()

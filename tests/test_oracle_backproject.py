@@ -103,3 +103,19 @@ def test_corrected_row_layout():
     full = corrected_row(row, 2)
     assert full.shape == (5 + 2 * H_CORR,)
     assert full[H_CORR + 2] == pytest.approx(np.dot(row, correction_filter(2)[H_CORR + 2 - np.arange(5)]))
+
+
+@pytest.mark.parametrize("zeta,ly,n_det", [(1.0, 1.0, 25), (0.0, 0.5, 47), (1.5, 1.0, 20), (0.5, 0.75, 31)])
+def test_backproject_pixels_equals_full(zeta, ly, n_det):
+    """backproject(pixels=...) (the sampled checker of full-size GPU back projections) against
+    the full-grid backproject at every pixel of an N = 16 image, in a shuffled pixel order."""
+    rng = np.random.default_rng(5)
+    ang = np.concatenate([np.arange(24) * np.pi / 24, rng.uniform(0, np.pi, 3)])
+    g = dict(N=16, lambda_x=1.0, angles=ang, lambda_y=ly, n_det=n_det, zeta=zeta)
+    sino = rng.uniform(-1, 1, (len(ang), n_det))
+    full = backproject(g, sino)
+    k1, k2 = np.meshgrid(np.arange(16), np.arange(16), indexing="ij")
+    perm = rng.permutation(256)
+    k1, k2 = k1.ravel()[perm], k2.ravel()[perm]
+    at = backproject(g, sino, pixels=(k1, k2))
+    assert np.abs(at - full[k1, k2]).max() <= 1e-14 * np.abs(full).max()

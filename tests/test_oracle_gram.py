@@ -90,3 +90,17 @@ def test_far_field_law():
     for r in (10, 20, 40, 80):
         m = (R >= r - 0.5) & (R < r + 0.5)
         assert (G[m] * np.pi * R[m] / n).mean() == pytest.approx(1.0, abs=5e-3)
+
+
+@pytest.mark.parametrize("zeta,lam,n", [(0.0, 1.0, 12), (1.0, 1.0, 30), (0.5, 0.7, 17)])
+def test_gram_taps_at_equals_full_filter(zeta, lam, n):
+    """gram_taps_at (the sampled checker of full-size GPU filters) against the pinned full
+    filter gram_taps at every offset of an N = 16 filter (irregular angles included)."""
+    rng = np.random.default_rng(11)
+    ang = np.concatenate([np.arange(n) * np.pi / n, rng.uniform(-1.0, 4.0, 3)])
+    g = geom(16, ang, zeta, lam)
+    full = gram_taps(g)
+    d1, d2 = np.meshgrid(np.arange(-15, 16), np.arange(-15, 16), indexing="ij")
+    from oracle.gram import gram_taps_at
+    at = gram_taps_at(g, d1.ravel(), d2.ravel()).reshape(full.shape)
+    assert np.abs(at - full).max() <= 1e-14 * np.abs(full).max()
