@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-cufft", action="store_true")
     ap.add_argument("--json-out", default=None)
+    ap.add_argument("--dense-angles", action="store_true",
+                    help="only the SURVEY.md 8(d) Gram-build pair (production vs dense-angle build) at this config "
+                         "and config 4, one JSON line")
     return ap.parse_args()
 
 
@@ -138,31 +141,57 @@ def dist_env():
 
 
 # ----------------------------------------------------------------------------- CPU oracle sample
-def oracle_sample(cfg, iters: int, bp_stride: int = 64, cg_iters: int | None = None):
-    """The FP64 oracle (as it stands) on one slice of the workload: Gram taps, back
-    projection of every bp_stride-th pixel (time extrapolated x bp_stride), and CG
-    iterations with the FFT apply.  Returns (slice-iterations/s, detail)."""
-    from oracle import solvers
-    from oracle.backproject import backproject
+# The FP64 oracle (oracle/, as it stands: never tuned) timed on the host cores: Gram taps and
+# back projection split over angle blocks in a multiprocessing.Pool(ncores) (both are sums over
+# angles), the CG iterations with SciPy's FFT on all cores (workers=-1 in
+# oracle.normal.apply_fft).  Bounded samples: a pixel subset of the back projection and a few CG
+# iterations, the times extrapolated to the whole slice and the configured iteration count.
+def _oracle_gram_block(args):
+    g, a0, a1 = args
     from oracle.gram import gram_taps
-    from synth.sinogram import config_sinogram
+    return gram_taps(g, a0, a1)
+
+
+def _oracle_bp_block(args):
+    g, sino, a0, a1, k1, k2 = args
+    from oracle.backproject import backproject
+    sub = dict(g)
+    sub["angles"] = np.asarray(g["angles"])[a0:a1]
+    return backproject(sub, sino[a0:a1], pixels=(k1, k2))
+
+
+def oracle_sample(cfg, iters: int, pool, ncores: int, bp_stride: int = 64, cg_iters: int | None = None):
+    """One slice of config `cfg` through the oracle: returns (slice-iterations/s of the whole
+    per-slice hot path, detail with the per-phase numbers)."""
+    from oracle import solvers
+    from synth.sinogram import random_sinogram
     g = cfg.geometry()
-    sino = config_sinogram(cfg, 0)
+    n = len(g["angles"])
+    sino = random_sinogram(cfg.seed, 1, n, cfg.n_det)[0]  # timing sample: the values do not matter
+    nb = max(1, min(ncores, n))
+    blocks = [(i * n // nb, (i + 1) * n // nb) for i in range(nb)]
     t0 = time.perf_counter()
-    T = gram_taps(g)
+    T = sum(pool.map(_oracle_gram_block, [(g, a0, a1) for a0, a1 in blocks]))
     t1 = time.perf_counter()
     N = cfg.N
     idx = np.arange(0, N * N, bp_stride)
-    b_s = backproject(g, sino, pixels=(idx // N, idx % N))
+    k1, k2 = idx // N, idx % N
+    b_s = sum(pool.map(_oracle_bp_block, [(g, sino, a0, a1, k1, k2) for a0, a1 in blocks]))
     t2 = time.perf_counter()
     b = np.zeros((N, N))
     b.flat[idx] = b_s
-    k = cg_iters or iters
+    k = min(cg_iters or iters, iters)
     solvers.cg(T, b, k)
     t3 = time.perf_counter()
-    t_slice = (t1 - t0) + (t2 - t1) * bp_stride + (t3 - t2) * iters / k
-    return iters / t_slice, dict(gram_s=t1 - t0, bp_s_extrapolated=(t2 - t1) * bp_stride,
-                                 cg_s=(t3 - t2) * iters / k, wall_s=t3 - t0)
+    bp_s = (t2 - t1) * bp_stride
+    cg_s = (t3 - t2) * iters / k
+    t_slice = (t1 - t0) + bp_s + cg_s
+    return iters / t_slice, dict(gram_ms=1e3 * (t1 - t0), bp_s_extrapolated=bp_s,
+                                 bp_gvox_angle_s=N * N * n / bp_s / 1e9, cg_s=cg_s,
+                                 cg_slice_iter_s=iters / cg_s, wall_s=t3 - t0,
+                                 sample=f"config {cfg.index}, 1 slice: Gram over {nb} angle blocks, back projection of "
+                                        f"every {bp_stride}th pixel (time x{bp_stride}), {k} of {iters} CG iterations "
+                                        f"(time x{iters}/{k})")
 
 
 def cpu_cores() -> int:
@@ -170,6 +199,123 @@ def cpu_cores() -> int:
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
+
+
+def oracle_pool(ncores: int):
+    import multiprocessing as mp
+    return mp.get_context("spawn").Pool(ncores)
+
+
+# bounded oracle samples per config (about 2-8 s each on 16 cores): (bp_stride, cg_iters)
+ORACLE_SAMPLES = {1: (4, 20), 2: (16, 10), 3: (64, 5), 4: (256, 3), 5: (32, 10)}
+
+
+# ----------------------------------------------------------------------------- GPU side measurements
+def device_ms(fn, reps: int = 20, warm: int = 3) -> float:
+    """Median device time of fn() (CUDA events), each call enqueued behind ~1 ms of device work
+    (torch.cuda._sleep) so that the events see the device time, not the host-side call cost."""
+    import torch
+    for _ in range(warm):
+        fn()
+    ts = []
+    for _ in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(2_000_000)
+        a.record()
+        fn()
+        b.record()
+        torch.cuda.synchronize()
+        ts.append(a.elapsed_time(b))
+    return float(np.median(ts))
+
+
+def gram_nonzero_pairs(g: dict, dev) -> int:
+    """Number of (tap, angle) pairs with |lambda_x <theta_perp, dk>| < W_t / 2 over the whole
+    (2N-1)^2 filter: the terms of P:122-129 that are not exactly zero (counted with torch)."""
+    import torch
+    N, lx, zeta = int(g["N"]), float(g.get("lambda_x", 1.0)), float(g.get("zeta", 0.0))
+    d = torch.arange(-(N - 1), N, device=dev, dtype=torch.float64)
+    a, b = d[:, None], d[None, :]
+    total = 0
+    for t in np.asarray(g["angles"], dtype=np.float64):
+        c, s_ = np.cos(t), np.sin(t)
+        H = lx * (abs(c) + abs(s_)) + zeta
+        total += int((torch.abs(lx * (-s_ * a + c * b)) < H).sum())
+    return total
+
+
+GRAM_OPS_PER_TERM = 25  # SURVEY.md 8(d): FP32 ops per nonzero evaluation (argument, piece search, Horner, add)
+
+
+def gram_pair(bsct, g: dict, dev, fma_peak_tflops: float, hbm_gbs: float) -> dict:
+    """SURVEY.md 8(d) Gram-build pair: (i) the production build (exact zeros skipped) as a fraction
+    of max(T_compute(nonzero evaluations), T_HBM(tap write)); (ii) the dense-angle build (every
+    (tap, angle) pair, BSCT_GRAM_DENSE=1) as an FP32 rate; the FP32-pipe utilisation of (ii)
+    comes from ncu (profiles/r02/ncu_gram_dense_*.txt, read here if present)."""
+    import glob
+
+    import torch
+    N, n = int(g["N"]), len(g["angles"])
+    D = 2 * N - 1
+    taps = torch.empty((D, D), device=dev)
+    ms = device_ms(lambda: bsct.gram_build(g, taps))
+    os.environ["BSCT_GRAM_DENSE"] = "1"
+    try:
+        ms_dense = device_ms(lambda: bsct.gram_build(g, taps), reps=5)
+    finally:
+        del os.environ["BSCT_GRAM_DENSE"]
+    nnz = gram_nonzero_pairs(g, dev)
+    t_comp = nnz * GRAM_OPS_PER_TERM / (fma_peak_tflops * 1e12) * 1e3
+    t_hbm = 4.0 * D * D / (hbm_gbs * 1e9) * 1e3
+    dense_terms = n * D * D
+    out = {"N": N, "n_angles": n, "build_ms": ms, "nonzero_pairs": nnz, "dense_pairs": dense_terms,
+           "work_ratio_dense_over_nonzero": dense_terms / max(nnz, 1),
+           "t_compute_ms": t_comp, "t_hbm_ms": t_hbm,
+           "frac_of_max_compute_hbm": max(t_comp, t_hbm) / ms,
+           "dense_build_ms": ms_dense,
+           "dense_fp32_tflops_algorithmic": dense_terms * GRAM_OPS_PER_TERM / (ms_dense / 1e3) / 1e12,
+           "dense_fp32_tflops_executed": 0.5 * dense_terms * GRAM_OPS_PER_TERM / (ms_dense / 1e3) / 1e12,
+           "dense_frac_of_fp32_peak_executed": 0.5 * dense_terms * GRAM_OPS_PER_TERM / (ms_dense / 1e3) / 1e12
+                                               / fma_peak_tflops,
+           "note": "build_ms = K0 tables + K1 taps (device time); FLOP model 25 FP32 ops per nonzero (tap, angle) "
+                   "term (SURVEY.md 8(d)); K1 evaluates the half of the taps up to the centre and mirrors "
+                   "(G[k] = G[-k]), so the dense mode executes dense_pairs / 2 terms"}
+    for mode in ("dense", "production"):  # ncu pipe utilisation (committed capture)
+        files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", f"ncu_gram_{mode}_N{N}.json")))
+        if files:
+            out[f"{mode}_ncu"] = json.load(open(files[-1]))
+            out[f"{mode}_ncu"]["source"] = os.path.relpath(files[-1], ROOT)
+    del taps
+    return out
+
+
+def per_config_gpu(bsct, dev, B: int = 16) -> dict:
+    """configs 1-4 on this GPU: Gram build (device ms), back projection (B slices) Gvox-angle/s and
+    CG slice-iterations/s at the config's iteration count, B = 1 and B = 16."""
+    import torch
+    out = {}
+    for ci in (1, 2, 3, 4):
+        c = CONFIGS[ci]
+        g = c.geometry()
+        dt = torch.float64 if c.dtype == "f64" else torch.float32
+        N, n, M = c.N, c.n_angles, c.n_det
+        taps = torch.empty((2 * N - 1, 2 * N - 1), dtype=dt, device=dev)
+        gm = device_ms(lambda: bsct.gram_build(g, taps), reps=10)
+        plan = bsct.plan_create(g, taps, max_batch=B)
+        gen = torch.Generator(device=dev).manual_seed(ci)
+        row = {"N": N, "dtype": c.dtype, "gram_build_ms": gm}
+        for nb in (1, B):
+            sino = torch.rand((nb, n, M), dtype=dt, device=dev, generator=gen)
+            b = torch.empty((nb, N, N), dtype=dt, device=dev)
+            x = torch.empty_like(b)
+            bp = device_ms(lambda: bsct.backproject(plan, sino, b), reps=5, warm=2)
+            cg = device_ms(lambda: bsct.cg_solve(plan, b, x, c.iters), reps=5, warm=2)
+            row[f"B{nb}"] = {"bp_ms": bp, "bp_gvox_angle_s": nb * N * N * n / (bp / 1e3) / 1e9,
+                             "cg_ms": cg, "cg_slice_iter_s": nb * c.iters / (cg / 1e3),
+                             "cg_us_per_slice_iter": 1e3 * cg / (nb * c.iters)}
+        out[ci] = row
+        del plan, taps
+    return out
 
 
 # ----------------------------------------------------------------------------- reference arm
@@ -180,27 +326,100 @@ def run_reference(args):
     cfg = CONFIGS[args.config]
     iters = args.iters or cfg.iters
     total = args.slices or cfg.n_slices
-    for _ in range(args.warmup):
-        oracle_sample(cfg, iters, bp_stride=256, cg_iters=5)
-    vals, det = [], None
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        v, det = oracle_sample(cfg, iters, bp_stride=256, cg_iters=5)
-        vals.append(v)
-    wall = time.perf_counter() - t0
+    ncores = cpu_cores()
+    stride, cgk = ORACLE_SAMPLES[args.config]
+    stride *= 4  # each step a smaller sample, so that --steps 20 --warmup 5 ends within minutes
+    with oracle_pool(ncores) as pool:
+        for _ in range(args.warmup):
+            oracle_sample(cfg, iters, pool, ncores, bp_stride=stride, cg_iters=cgk)
+        vals, det = [], None
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            v, det = oracle_sample(cfg, iters, pool, ncores, bp_stride=stride, cg_iters=cgk)
+            vals.append(v)
+        wall = time.perf_counter() - t0
     v = float(np.median(vals))
-    sample = (f"1 of {total} slices per step: Gram taps, back projection of every 256th pixel "
-              f"(time x256), 5 CG iterations (time x{iters}/5); FP64 NumPy/SciPy oracle")
+    sample = f"1 of {total} slices per step; {det['sample']}; FP64 NumPy/SciPy oracle, {ncores} processes"
     line = {"impl": "reference", "metric": "CG slice-iterations/s (full hot-path step) at N=512",
             "value": v, "unit": "slice-iterations/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * total * iters / v / max(args.gpus, 1),
+            "warmup": args.warmup, "ms_per_step": 1e3 * total * iters / v,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": f"BASELINE.json configs[{args.config}]", "N": cfg.N,
                                             "slices": total, "iters": iters},
-            "cpu_baseline": {"value": v, "unit": "slice-iterations/s", "cores": cpu_cores(), "kind": "oracle",
+            "cpu_baseline": {"value": v, "unit": "slice-iterations/s", "cores": ncores, "kind": "oracle",
                              "sample": sample, "detail": det, "wall_s": wall},
             "e2e": {"value": v, "unit": "slice-iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def fma_peak():
+    """Measured FP32 FMA peak (tools/fma_peak.cu on this pool's B200, profiles/*/fma_peak.json), else
+    148 SMs x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md)."""
+    import glob
+    fm = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "fma_peak.json")))
+    if fm:
+        return float(json.load(open(fm[-1]))["fp32_fma_tflops"]), \
+            f"measured: {os.path.relpath(fm[-1], ROOT)} (tools/fma_peak.cu, FP32 FMA chains)"
+    return fp32_peak_tflops(1965.0), "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md)"
+
+
+def roofline(per: dict, cfg, B: int, clk: dict, peaks: dict):
+    """Roofline of the dominant kernel class of one profiled step (library CUDA events around every
+    launch on its stream) and the HBM rooflines of the three FFT passes / whole CG iteration."""
+    N, n_ang, M = cfg.N, cfg.n_angles, cfg.n_det
+    L = 2
+    while L < 2 * N - 1:
+        L *= 2
+    Q = L // 2 + 1
+    dom = max(per, key=lambda k: per[k][0])
+    vox_angles = B * N * N * n_ang
+    # compulsory HBM bytes per launch of the fused CG passes (DESIGN.md 5): A reads p, r, x and
+    # writes x, p and T1; B reads and writes T1; C reads T1 and reads/writes r (CG mode)
+    cg_bytes = {"pass_a": B * (20 * N * N + 8 * Q * N), "pass_b": B * 16 * Q * N,
+                "pass_c": B * (8 * Q * N + 8 * N * N)}
+    kernels = {}
+    for kk in ("pass_a", "pass_b", "pass_c"):
+        if kk in per and per[kk][1] > 0:
+            ms1 = per[kk][0] / per[kk][1]
+            gbs = cg_bytes[kk] / (ms1 / 1e3) / 1e9
+            kernels[kk] = {"ms_per_launch": ms1, "bound": "hbm", "achieved_gbs": gbs,
+                           "frac_of_measured_hbm": gbs / peaks["hbm_gbs"]}
+    # the whole fused CG iteration (normal apply + updates): compulsory bytes / iteration time
+    if all(kk in kernels for kk in ("pass_a", "pass_b", "pass_c")):
+        it_ms = sum(kernels[kk]["ms_per_launch"] for kk in ("pass_a", "pass_b", "pass_c"))
+        it_bytes = sum(cg_bytes[kk] for kk in ("pass_a", "pass_b", "pass_c"))
+        kernels["cg_iteration"] = {"ms": it_ms, "bytes": it_bytes, "achieved_gbs": it_bytes / (it_ms / 1e3) / 1e9,
+                                   "frac_of_measured_hbm": it_bytes / (it_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                   "state_floor_bytes": B * 24 * N * N,
+                                   "frac_state_floor": B * 24 * N * N / (it_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
+                                   "note": "north_star: FFT normal-operator apply >= 60% of HBM roofline"}
+    if dom == "backproject":
+        # algorithmic FLOP per vox-angle (DESIGN.md K4): S_eff samples x (degree-5 Horner = 5 FMA
+        # + 1 FMA accumulate) x 2 flop + 2 FMA for k_theta; S_eff = mean support / lambda_y
+        w_mean = (4 / np.pi) * cfg.lambda_x + cfg.zeta + 3 * cfg.lambda_y
+        flops = vox_angles * (w_mean / cfg.lambda_y * 12.0 + 4.0)
+        ms_launch = per[dom][0] / max(per[dom][1], 1)
+        ach = flops / (ms_launch / 1e3) / 1e12
+        peak, peak_src = fma_peak()
+        tb, tsrc = ncu_traffic("bp_v3_kernel", B)
+        roof = {"kernel": "backproject (K4)", "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": tb, "traffic_source": tsrc,
+                "algorithmic_bytes": B * 4 * (n_ang * (M + 50) + N * N),
+                "peak_source": peak_src,
+                "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6); "
+                        "K4 evaluates it from per-tile tables and is shared-memory bound"}
+    else:
+        # HBM-bound FFT passes: compulsory bytes of the pass per launch (DESIGN.md K5)
+        byts = cg_bytes.get(dom, 0)
+        ms_launch = per[dom][0] / max(per[dom][1], 1)
+        ach = byts / (ms_launch / 1e3) / 1e9
+        kname = {"pass_a": "cg_pass_a_1024_kernel", "pass_b": "pass_b_1024_kernel",
+                 "pass_c": "cg_pass_c_1024_kernel"}.get(dom, dom)
+        tb, tsrc = ncu_traffic(kname, B)
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": ach / peaks["hbm_gbs"], "traffic": tb, "traffic_source": tsrc,
+                "peak_source": peaks["source"]}
+    return roof, kernels
 
 
 # ----------------------------------------------------------------------------- our arm
@@ -335,61 +554,9 @@ def run_ours(args):
     # ---- roofline of the dominant kernel class (profiler events inside the timed region)
     peaks = load_peaks()
     per = {k: (ms, cnt) for k, (ms, cnt) in prof.items()}  # one profiled step
-    dom = max(per, key=lambda k: per[k][0])
     L = plan.L
     Q = L // 2 + 1
-    vox_angles = B * N * N * n_ang
-    # compulsory HBM bytes per launch of the fused CG passes: A reads p, r, x and
-    # writes x, p and T1; B reads and writes T1; C reads T1 and reads/writes r (CG mode)
-    cg_bytes = {"pass_a": B * (20 * N * N + 8 * Q * N), "pass_b": B * 16 * Q * N,
-                "pass_c": B * (8 * Q * N + 8 * N * N),
-                "solver_update": B * 4 * N * N * 6, "solver_finish": B * 4 * N * N * 3}
-    kernels = {}
-    for kk in ("pass_a", "pass_b", "pass_c"):
-        if kk in per and per[kk][1] > 0:
-            ms1 = per[kk][0] / per[kk][1]
-            gbs = cg_bytes[kk] / (ms1 / 1e3) / 1e9
-            kernels[kk] = {"ms_per_launch": ms1, "bound": "hbm", "achieved_gbs": gbs,
-                           "frac_of_measured_hbm": gbs / peaks["hbm_gbs"]}
-    # the whole fused CG iteration (normal apply + updates): compulsory bytes / iteration time
-    if all(kk in kernels for kk in ("pass_a", "pass_b", "pass_c")):
-        it_ms = sum(kernels[kk]["ms_per_launch"] for kk in ("pass_a", "pass_b", "pass_c"))
-        it_bytes = sum(cg_bytes[kk] for kk in ("pass_a", "pass_b", "pass_c"))
-        kernels["cg_iteration"] = {"ms": it_ms, "bytes": it_bytes, "achieved_gbs": it_bytes / (it_ms / 1e3) / 1e9,
-                                   "frac_of_measured_hbm": it_bytes / (it_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
-                                   "note": "north_star: FFT normal-operator apply >= 60% of HBM roofline"}
-    if dom == "backproject":
-        # algorithmic FLOP per vox-angle (K4): S_eff samples x (degree-5 Horner = 5 FMA
-        # + 1 FMA accumulate) x 2 flop + 2 FMA for k_theta; S_eff = mean support / lambda_y
-        w_mean = (4 / np.pi) * cfg.lambda_x + cfg.zeta + 3 * cfg.lambda_y
-        flops = vox_angles * (w_mean / cfg.lambda_y * 12.0 + 4.0)
-        ms_launch = per[dom][0] / max(per[dom][1], 1)
-        ach = flops / (ms_launch / 1e3) / 1e12
-        peak, peak_src = fp32_peak_tflops(clk.get("sm_max_mhz") or 1965.0), \
-            "derived: 148 SMs x 128 FP32 lanes x 2 x sm_max_mhz (B200_PROFILING.md)"
-        import glob
-        fm = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "fma_peak.json")))
-        if fm:  # measured on this pool's B200 by tools/fma_peak.cu
-            peak = float(json.load(open(fm[-1]))["fp32_fma_tflops"])
-            peak_src = f"measured: {os.path.relpath(fm[-1], ROOT)} (tools/fma_peak.cu, FP32 FMA chains)"
-        tb, tsrc = ncu_traffic("bp_v3_kernel", B)
-        roof = {"kernel": "backproject (K4)", "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": tb, "traffic_source": tsrc,
-                "algorithmic_bytes": B * 4 * (n_ang * (M + 50) + N * N),
-                "peak_source": peak_src,
-                "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6); "
-                        "K4 v3 evaluates it from per-tile tables and is shared-memory bound (ncu L1/smem 84%)"}
-    else:
-        # HBM-bound FFT passes: compulsory bytes of the pass per launch (K5)
-        byts = cg_bytes.get(dom, 0)
-        ms_launch = per[dom][0] / max(per[dom][1], 1)
-        ach = byts / (ms_launch / 1e3) / 1e9
-        kname = {"pass_a": "cg_pass_a_1024_kernel", "pass_b": "pass_b_1024_kernel",
-                 "pass_c": "cg_pass_c_1024_kernel"}.get(dom, dom)
-        tb, tsrc = ncu_traffic(kname, B)
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": tb, "traffic_source": tsrc,
-                "peak_source": peaks["source"]}
+    roof, kernels = roofline(per, cfg, B, clk, peaks)
 
     # ---- side by side (comparison only, not a product path): y = G x through cuFFT
     # (torch.fft: rfft2 of the zero-padded L x L slice, * spectrum, irfft2, crop) against
@@ -514,13 +681,33 @@ def run_ours(args):
                  "sirt_iteration_ms": s_ms, "cg_iteration_ms": c_ms, "sirt_over_cg": s_ms / c_ms}
         del hs, ims, xs
 
+    # ---- SURVEY.md 8(d) Gram-build pair (this config's geometry and config 4's) and the per-config
+    # GPU numbers (configs 1-4; config 5 is this run)
+    gram = None
+    pcfg = None
+    if not args.no_cufft:
+        fpk, _ = fma_peak()
+        gram = {f"config{args.config}": gram_pair(bsct, g, dev, fpk, peaks["hbm_gbs"]),
+                "config4": gram_pair(bsct, CONFIGS[4].geometry(), dev, fpk, peaks["hbm_gbs"])}
+        pcfg = per_config_gpu(bsct, dev)
+
     cpu = None
     if not args.no_cpu and ws == 1:
-        v, det = oracle_sample(cfg, iters, bp_stride=16, cg_iters=iters)
-        cpu = {"value": v, "unit": "slice-iterations/s", "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"1 slice of config {args.config}: Gram taps, back projection of every 16th pixel "
-                         f"(time x16), {iters} CG iterations; FP64 NumPy/SciPy oracle as it stands",
-               "detail": det}
+        ncores = cpu_cores()
+        stride, cgk = ORACLE_SAMPLES[args.config]
+        with oracle_pool(ncores) as pool:
+            v, det = oracle_sample(cfg, iters, pool, ncores, bp_stride=stride, cg_iters=cgk)
+            per_cfg = {}
+            for ci in (1, 2, 3, 4):
+                c = CONFIGS[ci]
+                s_ci, k_ci = ORACLE_SAMPLES[ci]
+                _, d = oracle_sample(c, c.iters, pool, ncores, bp_stride=s_ci, cg_iters=k_ci)
+                per_cfg[ci] = {k: d[k] for k in ("gram_ms", "bp_gvox_angle_s", "cg_slice_iter_s", "sample")}
+            per_cfg[args.config] = {k: det[k] for k in ("gram_ms", "bp_gvox_angle_s", "cg_slice_iter_s", "sample")}
+        cpu = {"value": v, "unit": "slice-iterations/s", "cores": ncores, "kind": "oracle",
+               "sample": det["sample"] + f"; FP64 NumPy/SciPy oracle as it stands, Pool({ncores}) over angle "
+                                         f"blocks, SciPy FFT workers=-1",
+               "detail": det, "per_config": per_cfg}
 
     kernel_ms = {k: round(v[0], 4) for k, v in per.items()}
     line = {
@@ -535,7 +722,10 @@ def run_ours(args):
         "phases_ms": {"gram_build": phases[0], "set_filter": phases[1], "backproject": phases[2],
                       "cg_solve": phases[3],
                       "note": "separate profiled step (library events around every launch); the timed step calls bsct_reconstruct"},
-        "gram_build_ms": float(phases[0] + phases[1]),
+        "gram_build_ms": float(phases[0]),
+        "gram_build_plus_set_filter_ms": float(phases[0] + phases[1]),
+        "gram_pair": gram,
+        "per_config_gpu": pcfg,
         "backproj_gvox_angle_s": total * N * N * n_ang / (phases[2] / 1e3) / 1e9,
         "cg_only_slice_iter_s": total * iters / (phases[3] / 1e3),
         "kernel_ms_per_step": kernel_ms,
@@ -557,10 +747,204 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------- configs 1-4: one slice
+def run_single(args):
+    """BASELINE.json configs 1-4: one 2D slice.  The two angle sums shard over the ranks
+    (SURVEY.md 8(e)): each rank builds the Gram filter over its angle range, bsct_gram_build
+    (a2), and one NCCL allreduce sums the (2N-1)^2 partial filters (a3, BJ:configs[4]); the
+    back projection likewise (D6: each rank back projects its angle range, one allreduce of the
+    N^2 partial image).  The filter spectrum and the CG solve of the single slice do not shard
+    (replicas).  One step = gram shard + allreduce + set_filter + BP shard + allreduce + CG."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2005_13471_b200 as bsct
+    from paper_2005_13471_b200.parallel import angle_shard, angle_shard_geometry
+    from synth.sinogram import config_sinogram
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    bsct.load()
+    dev = torch.device("cuda", local)
+    cfg = CONFIGS[args.config]
+    iters = args.iters or cfg.iters
+    g = cfg.geometry()
+    N, n_ang, M = cfg.N, cfg.n_angles, cfg.n_det
+    dt = torch.float64 if cfg.dtype == "f64" else torch.float32
+    D = 2 * N - 1
+    ga0, ga1 = angle_shard(n_ang, ws, rank)
+    sub, ba0, ba1 = angle_shard_geometry(g, ws, rank)
+    taps = torch.empty((D, D), dtype=dt, device=dev)
+    bsct.gram_build(g, taps)
+    plan = bsct.plan_create(g, taps, max_batch=1)
+    plan_s = bsct.plan_create(sub, taps, max_batch=1) if ba1 > ba0 else None
+    sino_h = torch.from_numpy(config_sinogram(cfg, 0)[None].astype(np.float64 if cfg.dtype == "f64" else np.float32))
+    sino = sino_h.to(dev)
+    sino_s = sino[:, ba0:ba1].contiguous()
+    b = torch.empty((1, N, N), dtype=dt, device=dev)
+    x = torch.empty_like(b)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(7)]
+
+    def step(marks=False):
+        if marks:
+            ev[0].record()
+        bsct.gram_build(g, taps, ga0, ga1)  # this rank's angle shard (a2)
+        if marks:
+            ev[1].record()
+        if ws > 1:
+            dist.all_reduce(taps, op=dist.ReduceOp.SUM)  # a3 (same stream: ordered after the build)
+        if marks:
+            ev[2].record()
+        bsct.plan_set_filter(plan, taps)  # a1 + a4
+        if marks:
+            ev[3].record()
+        if plan_s is None:
+            b.zero_()
+        else:
+            bsct.backproject(plan_s, sino_s, b)  # a5 + a6 over this rank's angles (D6)
+        if marks:
+            ev[4].record()
+        if ws > 1:
+            dist.all_reduce(b, op=dist.ReduceOp.SUM)
+        if marks:
+            ev[5].record()
+        bsct.cg_solve(plan, b, x, iters, args.solver)  # a7 + a8
+        if marks:
+            ev[6].record()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    # library kernel launches per step: gram_build (K0 + K1), set_filter, back projection, solve
+    launches = 2
+    bsct.plan_set_filter(plan, taps)
+    launches += plan.launches
+    if plan_s is not None:
+        bsct.backproject(plan_s, sino_s, b)
+        launches += plan_s.launches
+    bsct.cg_solve(plan, b, x, iters, args.solver)
+    launches += plan.launches
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t_step = e0.elapsed_time(e1) / args.steps
+    # phase breakdown: the median of 10 marked steps
+    ph = []
+    for _ in range(10):
+        step(marks=True)
+        torch.cuda.synchronize()
+        ph.append([ev[i].elapsed_time(ev[i + 1]) for i in range(6)])
+    ph = np.median(np.array(ph), axis=0)
+    # e2e: the sinogram from pinned host memory and the reconstruction back, inside the timed region
+    sino_p = sino_h.pin_memory()
+    x_p = torch.empty((1, N, N), dtype=dt).pin_memory()
+
+    def step_e2e():
+        sino.copy_(sino_p, non_blocking=True)
+        sino_s.copy_(sino[:, ba0:ba1])
+        step()
+        x_p.copy_(x, non_blocking=True)
+
+    step_e2e()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        step_e2e()
+    e1.record()
+    torch.cuda.synchronize()
+    t_e2e = e0.elapsed_time(e1) / args.steps
+    tt = torch.tensor([t_step, t_e2e, *ph.tolist()], device=dev, dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_step, t_e2e, ph = float(tt[0]), float(tt[1]), tt[2:].cpu().numpy()
+    # kernel-class profile of one step (roofline of the dominant class)
+    plan.profile(True)
+    if plan_s is not None:
+        plan_s.profile(True)
+    step()
+    prof = plan.profile_read()
+    if plan_s is not None:
+        for k, v in plan_s.profile_read().items():
+            prof[k] = (prof.get(k, (0.0, 0))[0] + v[0], prof.get(k, (0.0, 0))[1] + v[1])
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+    peaks = load_peaks()
+    roof, kernels = roofline(prof, cfg, 1, clk, peaks)
+    line = {
+        "metric": f"CG slice-iterations/s (full hot-path step) at N={N}",
+        "value": iters / (t_step / 1e3), "unit": "slice-iterations/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": t_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": cfg.dtype, "data": "synthetic",
+        "config": {"workload": f"BASELINE.json configs[{args.config}]: one slice N={N}, {n_ang} angles, {M} bins, "
+                               f"lambda_y={cfg.lambda_y}, zeta={cfg.zeta}, {iters} {args.solver.upper()} iterations; "
+                               f"Gram build and back projection over {ws} angle shard(s) + NCCL allreduce",
+                   "N": N, "iters": iters, "solver": args.solver, "angle_shards": ws,
+                   "l2": "single slice: the working set is L2-resident (no flush; the Gram filter is rebuilt every step)"},
+        "phases_ms_max_over_ranks": {"gram_shard": ph[0], "gram_allreduce": ph[1], "set_filter": ph[2],
+                                     "backproject_shard": ph[3], "bp_allreduce": ph[4], "cg_solve": ph[5]},
+        "gram_build_ms": float(ph[0] + ph[1]),
+        "kernel_ms_per_step": {k: round(v[0], 4) for k, v in prof.items()},
+        "cg_pass_rooflines": kernels,
+        "roofline": roof,
+        "cpu_baseline": None,
+        "e2e": {"value": iters / (t_e2e / 1e3), "unit": "slice-iterations/s",
+                "h2d_bytes_per_step": int(sino_p.numel() * sino_p.element_size()),
+                "d2h_bytes_per_step": int(x_p.numel() * x_p.element_size()), "ms_per_step": t_e2e},
+        "gpu_launches": launches * args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if args.json_out:
+        open(args.json_out, "w").write(json.dumps(line) + "\n")
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def run_gram_pair(args):
+    """bench.py --dense-angles: the Gram-build pair alone."""
+    import torch
+
+    import paper_2005_13471_b200 as bsct
+    ws, rank, local = dist_env()
+    if rank != 0:
+        return
+    torch.cuda.set_device(local)
+    bsct.load()
+    dev = torch.device("cuda", local)
+    peaks = load_peaks()
+    fpk, fsrc = fma_peak()
+    out = {"metric": "Gram-filter build ms (production) and dense-angle FP32 rate", "fp32_peak_tflops": fpk,
+           "fp32_peak_source": fsrc, "hbm_gbs": peaks["hbm_gbs"]}
+    for ci in sorted({args.config, 4}):
+        if CONFIGS[ci].dtype != "f32":
+            continue
+        out[f"config{ci}"] = gram_pair(bsct, CONFIGS[ci].geometry(), dev, fpk, peaks["hbm_gbs"])
+    print(json.dumps(out), flush=True)
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
+    elif args.dense_angles:
+        run_gram_pair(args)
+    elif CONFIGS[args.config].n_slices == 1:
+        run_single(args)
     else:
         run_ours(args)
 

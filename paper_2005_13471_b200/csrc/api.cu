@@ -9,6 +9,8 @@
 #include <type_traits>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/bsct.h"
 #include "fft.cuh"
 #include "kernels.cuh"
@@ -18,6 +20,12 @@ using namespace bsct;
 namespace {
 
 thread_local std::string g_err;
+
+// NVTX range around every C entry point (header-only NVTX3; visible in nsys / ncu timelines)
+struct NvtxRange {
+  explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 bsct_status fail(bsct_status st, const char *fmt, ...) {
   char buf[512];
@@ -747,6 +755,7 @@ int32_t bsct_version(void) { return 100; }
 
 bsct_status bsct_chebyshev_solve(bsct_plan p, const void *b, void *x, int32_t B, int32_t iters, double lambda_min,
                                  double lambda_max, double *resid_hist, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_chebyshev_solve");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
@@ -768,6 +777,7 @@ bsct_status bsct_chebyshev_solve(bsct_plan p, const void *b, void *x, int32_t B,
 }
 
 bsct_status bsct_adjoint_project(bsct_plan p, const void *sino, void *img, int32_t B, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_adjoint_project");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;
@@ -779,6 +789,7 @@ bsct_status bsct_adjoint_project(bsct_plan p, const void *sino, void *img, int32
 }
 
 bsct_status bsct_sirt_solve(bsct_plan p, const void *sino, void *x, int32_t B, int32_t iters, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_sirt_solve");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
@@ -796,6 +807,7 @@ int32_t bsct_fft_size(int32_t N) { return N < 1 ? 0 : fft_size(N); }
 
 bsct_status bsct_gram_build(const bsct_geometry *g, bsct_dtype dt, int32_t angle_begin, int32_t angle_end, void *taps,
                             bsct_stream stream) {
+  NvtxRange nvtx_("bsct_gram_build");
   bsct_status st = validate(g, dt);
   if (st != BSCT_OK) return st;
   if (angle_begin < 0 || angle_end < angle_begin || angle_end > g->n_angles)
@@ -808,6 +820,7 @@ bsct_status bsct_gram_build(const bsct_geometry *g, bsct_dtype dt, int32_t angle
 
 bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *taps, int32_t max_batch,
                              bsct_plan *out, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_plan_create");
   if (!out) return fail(BSCT_EINVAL, "out is NULL");
   *out = nullptr;
   bsct_status st = validate(g, dt);
@@ -846,6 +859,7 @@ bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *
 }
 
 bsct_status bsct_plan_destroy(bsct_plan p) {
+  NvtxRange nvtx_("bsct_plan_destroy");
   if (!p) return BSCT_OK;
   void *bufs[] = {p->adj_ang, p->adj_B, p->sirt_R, p->sirt_C, p->sino_tmp,
                   p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->r, p->p, p->q,
@@ -896,6 +910,7 @@ bsct_status bsct_plan_profile_read(bsct_plan p, double *ms, int64_t *count, int3
 }
 
 bsct_status bsct_plan_set_filter(bsct_plan p, const void *taps, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_plan_set_filter");
   bsct_status st = check_plan(p, 0);
   if (st != BSCT_OK) return st;
   if (!taps) return fail(BSCT_EINVAL, "taps is NULL");
@@ -905,6 +920,7 @@ bsct_status bsct_plan_set_filter(bsct_plan p, const void *taps, bsct_stream stre
 }
 
 bsct_status bsct_plan_spectrum(bsct_plan p, void *out, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_plan_spectrum");
   bsct_status st = check_plan(p, 0);
   if (st != BSCT_OK) return st;
   if (!out) return fail(BSCT_EINVAL, "out is NULL");
@@ -914,6 +930,7 @@ bsct_status bsct_plan_spectrum(bsct_plan p, void *out, bsct_stream stream) {
 }
 
 bsct_status bsct_correction_filter(bsct_plan p, const void *sino, void *g_tilde, int32_t B, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_correction_filter");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;
@@ -934,6 +951,7 @@ bsct_status bsct_correction_filter(bsct_plan p, const void *sino, void *g_tilde,
 }
 
 bsct_status bsct_backproject(bsct_plan p, const void *sino, void *b, int32_t B, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_backproject");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;
@@ -945,6 +963,7 @@ bsct_status bsct_backproject(bsct_plan p, const void *sino, void *b, int32_t B, 
 }
 
 bsct_status bsct_normal_apply(bsct_plan p, const void *x, void *y, int32_t B, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_normal_apply");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;
@@ -957,6 +976,7 @@ bsct_status bsct_normal_apply(bsct_plan p, const void *x, void *y, int32_t B, bs
 
 bsct_status bsct_cg_solve(bsct_plan p, const void *b, void *x, int32_t B, int32_t iters, int32_t solver,
                           double *resid_hist, int32_t *flags, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_cg_solve");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
@@ -972,6 +992,7 @@ bsct_status bsct_cg_solve(bsct_plan p, const void *b, void *x, int32_t B, int32_
 
 bsct_status bsct_cg_resume(bsct_plan p, void *x, void *r, void *pdir, int32_t B, int32_t iters, int32_t solver,
                            double *alpha_last, double *resid_hist, int32_t *flags, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_cg_resume");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
@@ -987,6 +1008,7 @@ bsct_status bsct_cg_resume(bsct_plan p, void *x, void *r, void *pdir, int32_t B,
 }
 
 bsct_status bsct_forward_project(bsct_plan p, const void *c, void *sino, int32_t B, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_forward_project");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;
@@ -1136,6 +1158,7 @@ extern "C" {
 
 bsct_status bsct_reconstruct(bsct_plan p, const void *sino, void *x, int32_t B, int32_t iters, int32_t solver,
                              double *resid_hist, int32_t *flags, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_reconstruct");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (iters < 0) return fail(BSCT_EINVAL, "iters < 0");
@@ -1147,6 +1170,7 @@ bsct_status bsct_reconstruct(bsct_plan p, const void *sino, void *x, int32_t B, 
 
 bsct_status bsct_reconstruct_host(bsct_plan p, const void *sino_host, void *x_host, int32_t B, int32_t iters,
                                   int32_t solver, bsct_stream stream) {
+  NvtxRange nvtx_("bsct_reconstruct_host");
   bsct_status st = check_plan(p, B);
   if (st != BSCT_OK) return st;
   if (B == 0) return BSCT_OK;

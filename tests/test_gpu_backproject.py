@@ -198,3 +198,28 @@ def test_angle_sharded_backprojection(cuda_lib):
         assert torch.equal(out, full)
     finally:
         dist.destroy_process_group()
+
+
+def test_two_devices_one_process(cuda_lib):
+    """Per-device state (the correction filter q in __constant__ memory, the library memory pool,
+    the cached angle sets) must exist on every device a process uses: the same back projection and
+    Gram filter on device 0 and device 1 agree bitwise.  Needs two GPUs (skipped otherwise; the
+    round's GPU runs have one)."""
+    import torch
+    if torch.cuda.device_count() < 2:
+        pytest.skip("needs two GPUs")
+    N, n, M = 64, 40, 101
+    g = dict(N=N, lambda_x=1.0, angles=np.arange(n) * np.pi / n + 0.03, lambda_y=1.0, n_det=M, zeta=1.0)
+    sino = np.random.default_rng(3).uniform(0, 1, (1, n, M))
+    outs = []
+    for d in (0, 1, 0):
+        with torch.cuda.device(d):
+            taps = torch.empty((2 * N - 1, 2 * N - 1), device=f"cuda:{d}")
+            cuda_lib.gram_build(g, taps)
+            plan = cuda_lib.plan_create(g, taps, max_batch=1)
+            b = torch.empty((1, N, N), device=f"cuda:{d}")
+            cuda_lib.backproject(plan, torch.as_tensor(sino, dtype=torch.float32, device=f"cuda:{d}"), b)
+            torch.cuda.synchronize(d)
+            outs.append((taps.cpu(), b.cpu()))
+    for t, b in outs[1:]:
+        assert torch.equal(t, outs[0][0]) and torch.equal(b, outs[0][1])
