@@ -93,6 +93,9 @@ struct bsct_plan_s {
   int bp_maxp = 9;            // K4 v2 sub-intervals per detector cell (max over angles)
   bool solver_v1 = false;     // unfused 5-launch iteration (A/B testing only)
   bool bp_v3 = true;          // FP32: K4 v3 (slices per CTA); BSCT_BP_V2=1 selects v2 (A/B testing)
+  bool bp_tc = false;         // FP32: K4 v4 on the tensor cores (bp_tc.cu) where the geometry fits
+  int ldt = 0;                // row stride of g~ (K4 v4: a multiple of 4 floats for TMA)
+  void *gt_lo = nullptr;      // K4 v4: FP32 residual of the TF32-rounded g~
   // plain adjoint H^T and SIRT (NEXT-1): K4 tables without the interpolation widths, weights
   BPAngle *adj_ang = nullptr;
   void *adj_B = nullptr;
@@ -356,7 +359,7 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   const char *bp2 = getenv("BSCT_BP_V2");
   p->bp_v3 = !(bp2 && bp2[0] == '1');
   if (p->bp_cells > 0) {
-    CU(cudaMalloc((void **)&p->bp_ang, sizeof(BPAngle) * n));
+    CU(cudaMalloc((void **)&p->bp_ang, sizeof(BPAngle) * n + 64));  // + 64: K4 v4 stages 16-byte aligned copies
     CU(cudaMalloc(&p->bp_B, sizeof(T) * bp_table_floats(n)));
   }
   bsct_status st = plan_filter_t<T>(p, taps, s);
@@ -365,7 +368,9 @@ bsct_status plan_init_t(bsct_plan p, const void *taps, cudaStream_t s) {
   const size_t nn = (size_t)N * N;
   const size_t Bz = Bm > 0 ? Bm : 1;
   CU(cudaMalloc(&p->T1, sizeof(cplx<T>) * Q * N * Bz));
-  CU(cudaMalloc(&p->gt, sizeof(T) * (size_t)n * (M + 2 * HC) * Bz));
+  p->ldt = p->bp_tc ? ((M + 2 * HC + 3) & ~3) : (M + 2 * HC);
+  CU(cudaMalloc(&p->gt, sizeof(T) * (size_t)n * p->ldt * Bz));
+  if (p->bp_tc) CU(cudaMalloc(&p->gt_lo, sizeof(T) * (size_t)n * p->ldt * Bz));
   CU(cudaMalloc(&p->r, sizeof(T) * nn * Bz));
   CU(cudaMalloc(&p->p, sizeof(T) * nn * Bz));
   CU(cudaMalloc(&p->q, sizeof(T) * nn * Bz));
@@ -419,6 +424,16 @@ bsct_status normal_apply_t(bsct_plan p, const T *x, T *y, int B, double *gpart, 
 template <typename T>
 bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t s) {
   PPTables<T> bp = tables_of<T>(p->bp_mem, p->n_angles);
+  if (std::is_same<T, float>::value && p->bp_tc && p->bp_cells > 0) {
+    // K4 v4: the TF32 split of g~ (hi into gt, residual into gt_lo, rows padded to ldt for TMA), then
+    // the tensor-core product per angle (bp_tc.cu)
+    LAUNCH(p, BSCT_K_CORRECTION, 1,
+           (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s, (T *)p->gt_lo, p->ldt)));
+    LAUNCH(p, BSCT_K_BACKPROJECT, 1,
+           (backproject_tc(p->N, p->n_angles, p->M, B, p->bp_ang, (const float *)p->bp_B, (const float *)p->gt,
+                           (const float *)p->gt_lo, p->ldt, (float *)b, p->lx * p->lx * p->ly, s)));
+    return BSCT_OK;
+  }
   LAUNCH(p, BSCT_K_CORRECTION, 1, (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s)));
   const int sb = (p->bp_cells > 0 && p->bp_v3 && std::is_same<T, float>::value)
                      ? bp_v3_slices(B, p->bp_maxp, p->bp_cells) : 0;
@@ -840,6 +855,7 @@ bsct_status bsct_plan_create(const bsct_geometry *g, bsct_dtype dt, const void *
   p->dt = dt;
   p->max_batch = max_batch;
   p->bp_maxp = bp_v2_max_p(g->n_angles, g->angles, g->lambda_x, g->lambda_y, g->zeta_blur);
+  p->bp_tc = dt == BSCT_F32 && bp_tc_supported(g->n_angles, g->angles, g->lambda_x, g->lambda_y, g->zeta_blur);
   cudaStream_t s = (cudaStream_t)stream;
   cudaError_t e = cudaMalloc((void **)&p->angles, sizeof(double) * g->n_angles);
   if (e == cudaSuccess) e = cudaMemcpyAsync(p->angles, g->angles, sizeof(double) * g->n_angles, cudaMemcpyHostToDevice, s);
@@ -862,7 +878,7 @@ bsct_status bsct_plan_destroy(bsct_plan p) {
   NvtxRange nvtx_("bsct_plan_destroy");
   if (!p) return BSCT_OK;
   void *bufs[] = {p->adj_ang, p->adj_B, p->sirt_R, p->sirt_C, p->sino_tmp,
-                  p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->r, p->p, p->q,
+                  p->angles, p->bp_mem, p->fw_mem, p->S, p->tw, p->T1, p->gt, p->gt_lo, p->r, p->p, p->q,
                   p->sino_dev, p->b_dev, p->x_dev, p->spec_work, p->bp_ang, p->bp_B, p->alpha, p->gpart, p->rpart, p->tau, p->rho, p->flags};
   for (void *b : bufs)
     if (b) cudaFree(b);

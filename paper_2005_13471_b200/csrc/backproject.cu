@@ -60,9 +60,18 @@ static cudaError_t upload_q() {
 // degree test is per angle, hence uniform per CTA.
 constexpr int CR_ROWS = 8;
 
+// split != nullptr (FP32, K4 v4): gt receives the TF32-rounded value (cvt.rna) and split the exact
+// FP32 residual, both with row stride ldt (the 3xTF32 operands of the tensor-core back projection)
+__device__ __forceinline__ float tf32_round(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) correction_kernel(int n_angles, int M, int B, const int *__restrict__ degree,
-                                                         const T *__restrict__ sino, T *__restrict__ gt) {
+                                                         const T *__restrict__ sino, T *__restrict__ gt,
+                                                         T *__restrict__ split, int ldt) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T *rows = reinterpret_cast<T *>(smem_raw);  // [CR_ROWS][M + 4 HC], zero-extended by 2 HC each side
   __shared__ T qs[2 * HC + 1];
@@ -87,12 +96,22 @@ __global__ void __launch_bounds__(256) correction_kernel(int n_angles, int M, in
     } else {
       v = row[HC];
     }
-    gt[((size_t)(b0 + rr) * n_angles + a) * Mt + j] = v;
+    const size_t o = ((size_t)(b0 + rr) * n_angles + a) * ldt + j;
+    if (split) {
+      if constexpr (sizeof(T) == 4) {
+        const T hi = tf32_round(v);
+        gt[o] = hi;
+        split[o] = v - hi;
+      }
+    } else {
+      gt[o] = v;
+    }
   }
 }
 
 template <typename T>
-cudaError_t correction_filter(int n_angles, int M, int B, const int *degree, const T *sino, T *gt, cudaStream_t s) {
+cudaError_t correction_filter(int n_angles, int M, int B, const int *degree, const T *sino, T *gt, cudaStream_t s,
+                              T *split, int ldt) {
   cudaError_t e = upload_q();
   if (e != cudaSuccess) return e;
   const size_t sm = sizeof(T) * (size_t)CR_ROWS * (M + 4 * HC);
@@ -100,7 +119,9 @@ cudaError_t correction_filter(int n_angles, int M, int B, const int *degree, con
     e = cudaFuncSetAttribute(correction_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
-  correction_kernel<T><<<dim3(n_angles, (B + CR_ROWS - 1) / CR_ROWS), 256, sm, s>>>(n_angles, M, B, degree, sino, gt);
+  if (ldt <= 0) ldt = M + 2 * HC;
+  correction_kernel<T><<<dim3(n_angles, (B + CR_ROWS - 1) / CR_ROWS), 256, sm, s>>>(n_angles, M, B, degree, sino, gt,
+                                                                                     split, ldt);
   return cudaGetLastError();
 }
 
@@ -845,8 +866,10 @@ template cudaError_t backproject_v2<float>(int, int, int, int, const BPAngle *, 
                                            int, int, double, cudaStream_t);
 template cudaError_t backproject_v2<double>(int, int, int, int, const BPAngle *, const double *, const double *,
                                             double *, int, int, double, cudaStream_t);
-template cudaError_t correction_filter<float>(int, int, int, const int *, const float *, float *, cudaStream_t);
-template cudaError_t correction_filter<double>(int, int, int, const int *, const double *, double *, cudaStream_t);
+template cudaError_t correction_filter<float>(int, int, int, const int *, const float *, float *, cudaStream_t, float *,
+                                              int);
+template cudaError_t correction_filter<double>(int, int, int, const int *, const double *, double *, cudaStream_t,
+                                               double *, int);
 template cudaError_t backproject<float>(int, double, double, int, int, int, const double *, PPView<float>,
                                         const float *, float *, cudaStream_t);
 template cudaError_t backproject<double>(int, double, double, int, int, int, const double *, PPView<double>,

@@ -1,0 +1,448 @@
+// bp_tc.cu -- K4 v4: the back projection b = H^T g^ on the 5th-generation tensor
+// cores (tcgen05.mma kind::tf32, accumulator in TMEM, operands staged by TMA and by the CTA).
+//
+// Per angle t the back projection of a pixel is a short dot product with the corrected
+// sinogram row (K4 v1-v3):
+//     b_s[k] += sum_i g~_s[c_k + imin + i] Q_{p_k, i}(tau_k),   i = 0 .. S-1,
+// where (c_k, p_k, tau_k) locate pixel k's detector coordinate u_k = <theta_perp, x_k>/lambda_y
+// (cell, sub-interval, local coordinate) and Q_{p,i} are the degree-5 basis polynomials of the
+// box spline C_t = M_[l|c|, l|s|, zeta] U [lambda_y]^(d+1) (bp_tables_kernel).  For a tile of
+// 128 pixels (8 x 16) every pixel's samples lie in one window of K = 32 consecutive detector
+// samples [m_lo, m_lo + 32), so for SB = 128 slices at once the angle's contribution is a
+// dense product
+//     D[pixel][slice] += W_t[pixel][j] G_t[j][slice],   W_t[k][j] = Q_{p_k, j + m_lo - c_k - imin}(tau_k)
+// (zero outside the pixel's S samples), M = 128, N = 128, K = 32: four tcgen05.mma K-steps per
+// angle.  FP32 accuracy from TF32 inputs by the 3xTF32 split: W = W_hi + W_lo and
+// G = G_hi + G_lo with W_hi, G_hi rounded to TF32 (cvt.rna.tf32) and the lo parts exact FP32
+// residuals; D += W_hi G_hi + W_hi G_lo + W_lo G_hi (the dropped W_lo G_lo is <= 2^-22 |W||G|).
+// Accumulation in FP32 in TMEM over all angles, in angle order (fixed: deterministic).
+//
+// Roles (192 threads, one CTA per SM, NS-stage smem ring):
+//   warps 0-3  one thread per pixel: locate, evaluate the S basis polynomials (Horner on the
+//              angle's basis table), write the W_hi / W_lo rows in the canonical K-major
+//              SWIZZLE_128B layout, fence.proxy.async, arrive on full_w[s]; epilogue:
+//              tcgen05.ld of the pixel's TMEM lane (128 slice columns) -> b.
+//   warp 4     TMA producer: G_hi / G_lo tiles [128 slices][32 samples] of the angle by
+//              cp.async.bulk.tensor (3-D maps over g~_hi / g~_lo, SWIZZLE_128B, zero fill outside
+//              the detector and the batch), completion counted on full_g[s].
+//   warp 5     TMEM allocation; one elected thread issues the 12 MMAs per angle and
+//              tcgen05.commit -> empty[s] (releases the stage) / done (after the last angle).
+// Every mbarrier wait traps after ~2^26 polls instead of hanging.
+
+#include <cuda.h>
+
+#include <cstdio>
+
+#include <cmath>
+#include <cstdint>
+#include <cstdlib>
+#include <mutex>
+
+#include "kernels.cuh"
+
+namespace bsct {
+
+namespace {
+
+constexpr int TC_M = 128, TC_N = 128, TC_K = 32;  // pixels, slices, samples per angle
+constexpr int TC_TR = 8, TC_TCOL = 16;             // pixel tile: 8 rows x 16 columns
+constexpr int TC_NS = 3;                           // pipeline stages
+constexpr int TC_THREADS = 320;  // 8 W-producer warps, TMA warp, MMA warp
+constexpr int TC_ROWB = 128;                        // bytes per operand row (32 x FP32)
+constexpr int TC_OPB = TC_M * TC_ROWB;              // one operand tile: 16 KB
+constexpr int TC_STAGEB = 4 * TC_OPB;               // W_hi, W_lo, G_hi, G_lo
+constexpr int HCv = 25;                             // correction filter half-width (R8)
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+#ifdef BSCT_TC_DEBUG
+#define TC_DBG(...) printf(__VA_ARGS__)
+#else
+#define TC_DBG(...)
+#endif
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int who = 0, int a = 0) {
+  uint32_t done = 0;
+  long long it = 0;
+  while (true) {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (++it > (1ll << 26)) {  // a lost arrival: fail loudly instead of hanging the GPU
+      TC_DBG("bp_tc timeout: block (%d,%d,%d) thread %d who %d angle %d bar %u parity %u\n", blockIdx.x, blockIdx.y,
+             blockIdx.z, threadIdx.x, who, a, bar, parity);
+      __trap();
+    }
+  }
+}
+
+__device__ __forceinline__ float tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
+// canonical K-major SWIZZLE_128B operand: row r (0..127) of 128 bytes, 16-byte chunk q -> q ^ (r & 7)
+__device__ __forceinline__ uint32_t sw128(int r, int k) {
+  return (uint32_t)(r * TC_ROWB + ((((k >> 2) ^ (r & 7))) << 4) + ((k & 3) << 2));
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_128B: start >> 4, LBO = 1 (unused when swizzled),
+// SBO = 1024 B (8 rows x 128 B) >> 4, version 1 (sm_100), layout type 2 (128B swizzle)
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+  return (uint64_t)((saddr & 0x3FFFF) >> 4) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
+}
+
+// instruction descriptor kind::tf32: D F32 (bits 4-5 = 1), A, B TF32 (bits 7-9, 10-12 = 2),
+// both K-major, N >> 3 at bits 17-22, M >> 4 at bits 24-28
+constexpr uint32_t TC_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(TC_N >> 3) << 17) |
+                              ((uint32_t)(TC_M >> 4) << 24);
+
+__device__ __forceinline__ void umma_tf32(uint32_t dtmem, uint64_t adesc, uint64_t bdesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dtmem),
+      "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accumulate));
+}
+
+__device__ __forceinline__ void umma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int x, int y, int z, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(dst),
+      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
+      : "memory");
+}
+
+}  // namespace
+
+// Shared memory per stage: W_hi, W_lo, G_hi, G_lo (16 KB each, 1024-aligned), the angle's basis
+// table B[p][i][8] (BP_PMAX x BP_SMAX x 8 floats) and its BPAngle record, both staged by bulk copy
+// with the G tiles (one mbarrier, full_g).
+constexpr int TC_TABB = BP_PMAX * BP_SMAX * 8 * 4;   // basis table bytes
+constexpr int TC_ANGB = (int)((sizeof(BPAngle) + 8 + 15) & ~(size_t)15);  // BPAngle + up to 8 B of misalignment
+constexpr int TC_STAGE = ((4 * TC_OPB + TC_TABB + TC_ANGB) + 1023) & ~1023;
+constexpr int TC_PROD = 256;  // producer threads: pixel t & 127, row half t >> 7
+
+__device__ __forceinline__ void st_shared_v4z(uint32_t a) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %1, %1, %1};" ::"r"(a), "f"(0.f) : "memory");
+}
+__device__ __forceinline__ void st_shared_f32(uint32_t a, float v) {
+  asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ float4 ld_shared_v4(uint32_t a) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// the tile's 32-sample window start m_lo for one angle: the lowest cell over the 8 x 16 tile minus
+// one (rounding margin) plus imin, aligned down so that column m_lo + HC is a multiple of 4 floats
+// (TMA box starts must be 16-byte aligned in the innermost dimension: an unaligned start raised an
+// illegal-instruction fault on B200)
+__device__ __forceinline__ int tc_window(double u0, double du1, double du2, int imin, int tk1, int tk2) {
+  const double ut = fma(du1, (double)tk1, fma(du2, (double)tk2, u0));
+  const double umin = ut + fmin(0.0, du1 * (TC_TR - 1)) + fmin(0.0, du2 * (TC_TCOL - 1));
+  return ((((int)floor(umin)) - 1 + imin + HCv) & ~3) - HCv;
+}
+
+__device__ __forceinline__ void st_shared_v4(uint32_t a, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(a), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
+}
+// the tensor cores read TF32 operands by ignoring the low 13 mantissa bits (measured: with raw FP32
+// operands and lo = x - trunc(x) the 3xTF32 product is as accurate as with pre-rounded hi parts), so
+// hi = x as stored and lo = x - trunc_tf32(x) (exact in FP32)
+__device__ __forceinline__ float tf32_lo(float x) { return x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Accumulation: the tensor cores' FP32 accumulation over many MMAs drifts (measured 3e-5 relative
+// after 360 angles x 12 MMAs against the CUDA-core K4 v3), so each block of TC_F angles is
+// accumulated from zero in one of two TMEM buffers (ping-pong, 2 x 128 columns) and the producer
+// threads add every finished block into FP32 registers (round to nearest), one block behind.
+constexpr int TC_F = 8;
+
+// grid (ceil(N/16), ceil(N/8), ceil(B/128)); 320 threads; dynamic smem = TC_NS stages + barriers + 1 KB
+__global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angles, int B,
+                                                              const BPAngle *__restrict__ ang,
+                                                              const float *__restrict__ Btab,
+                                                              const __grid_constant__ CUtensorMap map_g,
+                                                              const __grid_constant__ CUtensorMap map_lo,
+                                                              float *__restrict__ out, float scale) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t pad = (1024u - (raw & 1023u)) & 1023u;
+  unsigned char *smg = smem_raw + pad;  // generic view (shared window) of the aligned base
+  const uint32_t sm = raw + pad;        // 32-bit shared address of the aligned base
+  const uint32_t barb = sm + TC_NS * TC_STAGE;  // barriers after the stages
+  const uint32_t full_w = barb, full_g = barb + 8 * TC_NS, empty = barb + 16 * TC_NS;
+  const uint32_t acc_full = barb + 24 * TC_NS, acc_empty = acc_full + 16;
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smg + TC_NS * TC_STAGE + 24 * TC_NS + 32);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int tk1 = blockIdx.y * TC_TR, tk2 = blockIdx.x * TC_TCOL;
+  const int b0 = blockIdx.z * TC_N;
+  const int nblk = (n_angles + TC_F - 1) / TC_F;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < TC_NS; ++s) {
+      mbar_init(full_w + 8 * s, TC_PROD);
+      mbar_init(full_g + 8 * s, 1);
+      mbar_init(empty + 8 * s, 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(acc_full + 8 * b, 1);
+      mbar_init(acc_empty + 8 * b, TC_PROD);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 9) {  // TMEM: 2 x 128 columns (ping-pong FP32 accumulators, N = 128), owned by this warp
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_sh)),
+                 "n"(2 * TC_N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_sh;
+
+  if (warp < 8) {
+    // ---------------------------------------------------------------- W producers: pixel r, chunks [4h, 4h + 4)
+    const int t = threadIdx.x, r = t & 127, h = t >> 7;
+    const int k1 = tk1 + r / TC_TCOL, k2 = tk2 + r % TC_TCOL;
+    const bool inside = k1 < N && k2 < N;
+    float acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+    const uint32_t tlane = (uint32_t)((warp & 3) * 32) << 16;
+    auto flush = [&](int jf) {  // add TMEM block jf (columns [64 h, 64 h + 64) of lane r) into acc
+      const int buf = jf & 1;
+      mbar_wait(acc_full + 8 * buf, (uint32_t)((jf >> 1) & 1), 6, jf);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem + tlane + (uint32_t)(buf * TC_N + 64 * h + 32 * c), v);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) acc[32 * c + j] += __uint_as_float(v[j]);
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(acc_empty + 8 * buf);
+    };
+    int next_flush = 0;
+    for (int a = 0; a < n_angles; ++a) {
+      const int s = a % TC_NS;
+      const uint32_t par = (uint32_t)((a / TC_NS) & 1);
+      const uint32_t st = sm + s * TC_STAGE;
+      const uint32_t whi = st, wlo = st + TC_OPB, tab = st + 4 * TC_OPB;
+      mbar_wait(full_g + 8 * s, par, 1, a);  // G tiles, basis table and BPAngle of angle a have landed
+      const size_t aoff = (size_t)((uintptr_t)(ang + a) & 15);  // the staged copy starts 16-byte aligned
+      const BPAngle &A = *reinterpret_cast<const BPAngle *>(smg + s * TC_STAGE + 4 * TC_OPB + TC_TABB + aoff);
+      const int m_lo = tc_window(A.u0, A.du1, A.du2, A.imin, tk1, tk2);
+      const double u = fma(A.du1, (double)k1, fma(A.du2, (double)k2, A.u0));
+      const double cu = floor(u);
+      const float ph = (float)(u - cu);
+      const int P = A.P, S = A.S;
+      int p = 0;
+      for (int k = 1; k < P; ++k) p += ph >= (float)A.bp[k] ? 1 : 0;
+      const float tau = ph - (float)A.bp[p];
+      const int o = (int)cu + A.imin - m_lo;  // window position of sample i = 0
+      const int ilo = A.ilo[p], ihi = min((int)A.ihi[p], S - 1);
+      // zero this thread's half of the pixel's W_hi / W_lo rows, then its weights
+#pragma unroll
+      for (int q = 4 * h; q < 4 * h + 4; ++q) {  // logical chunk q of the row sits at chunk q ^ (r & 7)
+        st_shared_v4z(whi + r * TC_ROWB + ((q ^ (r & 7)) << 4));
+        st_shared_v4z(wlo + r * TC_ROWB + ((q ^ (r & 7)) << 4));
+      }
+      if (inside) {
+        const uint32_t bp = tab + (uint32_t)(p * BP_SMAX * 8 * 4);
+        for (int i = ilo; i <= ihi; ++i) {
+          const int pos = o + i;
+          if ((pos >> 4) != h) continue;  // the other half-row thread owns this position
+          const float4 c03 = ld_shared_v4(bp + i * 32), c47 = ld_shared_v4(bp + i * 32 + 16);
+          float w = c47.y;
+          w = fmaf(w, tau, c47.x);
+          w = fmaf(w, tau, c03.w);
+          w = fmaf(w, tau, c03.z);
+          w = fmaf(w, tau, c03.y);
+          w = fmaf(w, tau, c03.x);
+          const uint32_t off = sw128(r, pos);
+          st_shared_f32(whi + off, w);
+          st_shared_f32(wlo + off, tf32_lo(w));
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy (MMA)
+      mbar_arrive(full_w + 8 * s);
+      // block jf is flushed once block jf + 1 is fully produced (its MMAs are then long done)
+      while (next_flush + 2 <= (a + 1) / TC_F) flush(next_flush++);
+    }
+    while (next_flush < nblk) flush(next_flush++);
+    // ---------------------------------------------------------------- epilogue: acc -> b[:, k1, k2]
+    if (inside) {
+#pragma unroll
+      for (int j = 0; j < 64; ++j) {
+        const int b = b0 + 64 * h + j;
+        if (b < B) out[((size_t)b * N + k1) * N + k2] = scale * acc[j];
+      }
+    }
+  } else if (warp == 8) {
+    // ---------------------------------------------------------------- TMA producer
+    if (lane == 0) {
+      // this angle's window and sub-interval count from its BPAngle (global, prefetched one angle ahead)
+      double u0 = ang[0].u0, du1 = ang[0].du1, du2 = ang[0].du2;
+      int imin = ang[0].imin, P = ang[0].P;
+      for (int a = 0; a < n_angles; ++a) {
+        const int s = a % TC_NS;
+        const uint32_t par = (uint32_t)((a / TC_NS) & 1);
+        const int m_lo = tc_window(u0, du1, du2, imin, tk1, tk2);
+        const uint32_t tab_bytes = (uint32_t)(P * BP_SMAX * 8 * 4);  // rows of the P sub-intervals only
+        if (a + 1 < n_angles) {
+          u0 = ang[a + 1].u0;
+          du1 = ang[a + 1].du1;
+          du2 = ang[a + 1].du2;
+          imin = ang[a + 1].imin;
+          P = ang[a + 1].P;
+        }
+        mbar_wait(empty + 8 * s, par ^ 1, 2, a);
+        const uint32_t st = sm + s * TC_STAGE;
+        const char *asrc = reinterpret_cast<const char *>(ang + a);
+        const char *aal = reinterpret_cast<const char *>((uintptr_t)asrc & ~(uintptr_t)15);
+        mbar_expect_tx(full_g + 8 * s, 2 * TC_OPB + tab_bytes + TC_ANGB);
+        bulk_g2s(st + 4 * TC_OPB, Btab + (size_t)a * BP_PMAX * BP_SMAX * 8, tab_bytes, full_g + 8 * s);
+        bulk_g2s(st + 4 * TC_OPB + TC_TABB, aal, TC_ANGB, full_g + 8 * s);
+        // sample m <-> column m + HC of the corrected rows; outside the rows / batch: zero fill
+        tma_load_3d(st + 2 * TC_OPB, &map_g, m_lo + HCv, a, b0, full_g + 8 * s);
+        tma_load_3d(st + 3 * TC_OPB, &map_lo, m_lo + HCv, a, b0, full_g + 8 * s);
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- MMA issuer (one thread)
+    if (lane == 0) {
+      for (int a = 0; a < n_angles; ++a) {
+        const int s = a % TC_NS;
+        const uint32_t par = (uint32_t)((a / TC_NS) & 1);
+        const int j = a / TC_F, buf = j & 1;
+        const bool first = a % TC_F == 0, last = a % TC_F == TC_F - 1 || a == n_angles - 1;
+        if (first && j >= 2) mbar_wait(acc_empty + 8 * buf, (uint32_t)(((j - 2) >> 1) & 1), 7, a);
+        mbar_wait(full_w + 8 * s, par, 3, a);  // implies full_g (the producers waited on it)
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t st = sm + s * TC_STAGE;
+        const uint32_t whi = st, wlo = st + TC_OPB, ghi = st + 2 * TC_OPB, glo = st + 3 * TC_OPB;
+        const uint32_t As[3] = {whi, whi, wlo}, Bs[3] = {ghi, glo, ghi};
+        const uint32_t d = tmem + (uint32_t)(buf * TC_N);
+#pragma unroll
+        for (int pr = 0; pr < 3; ++pr)
+#pragma unroll
+          for (int kk = 0; kk < TC_K / 8; ++kk)  // K = 8 TF32 (32 bytes) per instruction
+            umma_tf32(d, umma_desc(As[pr] + 32 * kk), umma_desc(Bs[pr] + 32 * kk),
+                      (!first || pr > 0 || kk > 0) ? 1u : 0u);
+        umma_commit(empty + 8 * s);  // the stage is free once these MMAs have read it
+        if (last) umma_commit(acc_full + 8 * buf);  // block j complete in TMEM buffer j & 1
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 9) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(2 * TC_N));
+  }
+}
+
+// ------------------------------------------------------------------------------------ host side
+namespace {
+
+using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiled encoder() {
+  static EncodeTiled fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiled>(p);
+  });
+  return fn;
+}
+
+// 3-D map over rows [B][n_angles][ldt] FP32 (Mt valid columns): box {32, 1, 128}, SWIZZLE_128B
+bool make_map(CUtensorMap *map, const float *base, int Mt, int ldt, int n_angles, int B) {
+  EncodeTiled enc = encoder();
+  if (!enc) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)Mt, (cuuint64_t)n_angles, (cuuint64_t)B};
+  const cuuint64_t strides[2] = {(cuuint64_t)ldt * 4, (cuuint64_t)ldt * 4 * n_angles};
+  const cuuint32_t box[3] = {(cuuint32_t)TC_K, 1, (cuuint32_t)TC_N};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+}  // namespace
+
+// Geometry check (host, per plan): every 8 x 16 tile's samples fit the K = 32 window at every
+// angle: ceil(7 |du1| + 15 |du2|) + 1 (margin) + 1 (floor) + 3 (16-byte aligned start) + S <= 32,
+// du = lambda_x / lambda_y (sin, cos).
+bool bp_tc_supported(int n, const double *angles, double lx, double ly, double zeta) {
+  if (getenv("BSCT_BP_V3") && getenv("BSCT_BP_V3")[0] == '1') return false;
+  for (int i = 0; i < n; ++i) {
+    const double c = std::fabs(std::cos(angles[i])), s = std::fabs(std::sin(angles[i]));
+    const double span = (lx / ly) * ((TC_TR - 1) * s + (TC_TCOL - 1) * c);
+    const double H = 0.5 * (lx * (c + s) + zeta + 3.0 * ly);  // >= the half support of C_t
+    const int cw = (int)std::ceil(H / ly - 1e-12);
+    if ((int)std::ceil(span) + 2 + 3 + (2 * cw + 1) > TC_K) return false;  // + 3: aligned window start
+  }
+  return true;
+}
+
+size_t bp_tc_smem() { return (size_t)TC_NS * TC_STAGE + 24 * TC_NS + 64 + 1024; }
+
+cudaError_t backproject_tc(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
+                           const float *gt_lo, int ldt, float *out, double scale, cudaStream_t s) {
+  if (B <= 0) return cudaSuccess;
+  CUtensorMap mg, ml;
+  const int Mt = M + 2 * HCv;
+  if (!make_map(&mg, gt, Mt, ldt, n_angles, B) || !make_map(&ml, gt_lo, Mt, ldt, n_angles, B))
+    return cudaErrorNotSupported;
+  const size_t sm = bp_tc_smem();
+  cudaError_t e = cudaFuncSetAttribute(bp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  dim3 grid((N + TC_TCOL - 1) / TC_TCOL, (N + TC_TR - 1) / TC_TR, (B + TC_N - 1) / TC_N);
+  bp_tc_kernel<<<grid, TC_THREADS, sm, s>>>(N, n_angles, B, ang, Btab, mg, ml, out, (float)scale);
+  return cudaGetLastError();
+}
+
+}  // namespace bsct
