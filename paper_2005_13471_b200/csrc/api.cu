@@ -431,7 +431,7 @@ bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t 
            (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s, (T *)p->gt_lo, p->ldt)));
     LAUNCH(p, BSCT_K_BACKPROJECT, 1,
            (backproject_tc(p->N, p->n_angles, p->M, B, p->bp_ang, (const float *)p->bp_B, (const float *)p->gt,
-                           (const float *)p->gt_lo, p->ldt, (float *)b, p->lx * p->lx * p->ly, s)));
+                           (const float *)p->gt_lo, p->ldt, (float *)b, p->lx * p->lx * p->ly, p->bp_maxp, s)));
     return BSCT_OK;
   }
   LAUNCH(p, BSCT_K_CORRECTION, 1, (correction_filter<T>(p->n_angles, p->M, B, bp.degree, sino, (T *)p->gt, s)));

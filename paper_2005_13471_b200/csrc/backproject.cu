@@ -247,6 +247,7 @@ __global__ void __launch_bounds__(128) bp_tables_kernel(int N, int M, double lx,
     A.du1 = -s * lx / ly;
     A.du2 = c * lx / ly;
     for (int i = 0; i < BP_PMAX; ++i) A.bp[i] = i < np ? bp[i] : 3.0e38;
+    for (int i = 0; i < BP_PMAX; ++i) A.bpf[i] = i < np ? (float)bp[i] : 3.0e38f;
     A.P = np;
     A.S = S;
     A.imin = -cw;

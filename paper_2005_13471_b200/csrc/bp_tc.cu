@@ -46,11 +46,9 @@ namespace {
 
 constexpr int TC_M = 128, TC_N = 128, TC_K = 32;  // pixels, slices, samples per angle
 constexpr int TC_TR = 8, TC_TCOL = 16;             // pixel tile: 8 rows x 16 columns
-constexpr int TC_NS = 3;                           // pipeline stages
 constexpr int TC_THREADS = 320;  // 8 W-producer warps, TMA warp, MMA warp
 constexpr int TC_ROWB = 128;                        // bytes per operand row (32 x FP32)
 constexpr int TC_OPB = TC_M * TC_ROWB;              // one operand tile: 16 KB
-constexpr int TC_STAGEB = 4 * TC_OPB;               // W_hi, W_lo, G_hi, G_lo
 constexpr int HCv = 25;                             // correction filter half-width (R8)
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -132,12 +130,19 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
 
 }  // namespace
 
-// Shared memory per stage: W_hi, W_lo, G_hi, G_lo (16 KB each, 1024-aligned), the angle's basis
-// table B[p][i][8] (BP_PMAX x BP_SMAX x 8 floats) and its BPAngle record, both staged by bulk copy
-// with the G tiles (one mbarrier, full_g).
-constexpr int TC_TABB = BP_PMAX * BP_SMAX * 8 * 4;   // basis table bytes
-constexpr int TC_ANGB = (int)((sizeof(BPAngle) + 8 + 15) & ~(size_t)15);  // BPAngle + up to 8 B of misalignment
-constexpr int TC_STAGE = ((4 * TC_OPB + TC_TABB + TC_ANGB) + 1023) & ~1023;
+// Shared memory: three rings, so that the G tiles' L2 latency overlaps the weight production:
+//   tables  TC_NT slots: the angle's basis table (per-p rows padded to TC_PSTR bytes: lanes at the
+//           same row i but different sub-intervals p land in different banks) + its BPAngle record,
+//           bulk-copied; released by the producers (t_empty) once they have built W.
+//   W       TC_NW slots of W_hi, W_lo (16 KB each); released by the MMAs (w_empty).
+//   G       TC_NG slots of G_hi, G_lo (16 KB each), TMA; released by the MMAs (g_empty).
+constexpr int TC_PSTR = BP_SMAX * 8 * 4 + 16;                 // bytes per sub-interval in smem
+constexpr int TC_TABB = BP_PMAX * TC_PSTR;                     // basis table slot
+constexpr int TC_ANGB = (int)((sizeof(BPAngle) + 8 + 15) & ~(size_t)15);  // BPAngle + up to 8 B misalignment
+constexpr int TC_TSLOT = (TC_TABB + TC_ANGB + 127) & ~127;
+constexpr int TC_NT = 4, TC_NW = 3, TC_NG = 3;
+constexpr int TC_WOFF = 0, TC_GOFF = TC_NW * 2 * TC_OPB, TC_TOFF = TC_GOFF + TC_NG * 2 * TC_OPB;
+constexpr int TC_BOFF = (TC_TOFF + TC_NT * TC_TSLOT + 127) & ~127;  // barriers
 constexpr int TC_PROD = 256;  // producer threads: pixel t & 127, row half t >> 7
 
 __device__ __forceinline__ void st_shared_v4z(uint32_t a) {
@@ -192,32 +197,48 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t *v) {
 // accumulated from zero in one of two TMEM buffers (ping-pong, 2 x 128 columns) and the producer
 // threads add every finished block into FP32 registers (round to nearest), one block behind.
 constexpr int TC_F = 8;
+#ifdef BSCT_TC_TRACE
+__device__ long long g_tc_trace[8][512];
+#define TC_TR_MARK(slot, a) \
+  if (blockIdx.x == 7 && blockIdx.y == 20 && blockIdx.z == 3 && (a) < 512) g_tc_trace[slot][a] = clock64();
+#else
+#define TC_TR_MARK(slot, a)
+#endif
 
-// grid (ceil(N/16), ceil(N/8), ceil(B/128)); 320 threads; dynamic smem = TC_NS stages + barriers + 1 KB
+// grid (ceil(N/16), ceil(N/8), ceil(B/128)); 320 threads; dynamic smem = bp_tc_smem()
 __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angles, int B,
                                                               const BPAngle *__restrict__ ang,
                                                               const float *__restrict__ Btab,
                                                               const __grid_constant__ CUtensorMap map_g,
                                                               const __grid_constant__ CUtensorMap map_lo,
-                                                              float *__restrict__ out, float scale) {
+                                                              float *__restrict__ out, float scale, int maxP) {
   extern __shared__ __align__(1024) unsigned char smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t pad = (1024u - (raw & 1023u)) & 1023u;
   unsigned char *smg = smem_raw + pad;  // generic view (shared window) of the aligned base
   const uint32_t sm = raw + pad;        // 32-bit shared address of the aligned base
-  const uint32_t barb = sm + TC_NS * TC_STAGE;  // barriers after the stages
-  const uint32_t full_w = barb, full_g = barb + 8 * TC_NS, empty = barb + 16 * TC_NS;
-  const uint32_t acc_full = barb + 24 * TC_NS, acc_empty = acc_full + 16;
-  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smg + TC_NS * TC_STAGE + 24 * TC_NS + 32);
+  const uint32_t barb = sm + TC_BOFF;
+  // barriers: full_t/t_empty [NT], full_w/w_empty [NW], full_g/g_empty [NG], acc_full/acc_empty [2]
+  const uint32_t full_t = barb, t_empty = full_t + 8 * TC_NT, full_w = t_empty + 8 * TC_NT, w_empty = full_w + 8 * TC_NW,
+                 full_g = w_empty + 8 * TC_NW, g_empty = full_g + 8 * TC_NG, acc_full = g_empty + 8 * TC_NG,
+                 acc_empty = acc_full + 16;
+  uint32_t *tmem_sh = reinterpret_cast<uint32_t *>(smg + TC_BOFF + 8 * (2 * TC_NT + 2 * TC_NW + 2 * TC_NG + 4));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int tk1 = blockIdx.y * TC_TR, tk2 = blockIdx.x * TC_TCOL;
   const int b0 = blockIdx.z * TC_N;
   const int nblk = (n_angles + TC_F - 1) / TC_F;
   if (threadIdx.x == 0) {
-    for (int s = 0; s < TC_NS; ++s) {
-      mbar_init(full_w + 8 * s, TC_PROD);
+    for (int s = 0; s < TC_NT; ++s) {
+      mbar_init(full_t + 8 * s, 1);
+      mbar_init(t_empty + 8 * s, TC_PROD / 2);
+    }
+    for (int s = 0; s < TC_NW; ++s) {
+      mbar_init(full_w + 8 * s, TC_PROD / 2);
+      mbar_init(w_empty + 8 * s, 1);
+    }
+    for (int s = 0; s < TC_NG; ++s) {
       mbar_init(full_g + 8 * s, 1);
-      mbar_init(empty + 8 * s, 1);
+      mbar_init(g_empty + 8 * s, 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(acc_full + 8 * b, 1);
@@ -236,22 +257,25 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
   const uint32_t tmem = *tmem_sh;
 
   if (warp < 8) {
-    // ---------------------------------------------------------------- W producers: pixel r, chunks [4h, 4h + 4)
-    const int t = threadIdx.x, r = t & 127, h = t >> 7;
+    // ---------------------------------------------------------------- W producers
+    // two groups of 128 threads (warps 0-3, 4-7) take alternate angles, one thread per pixel row,
+    // so that two angles' locate / basis-evaluation latency chains are in flight at once
+    const int t = threadIdx.x, r = t & 127, grp = t >> 7;
     const int k1 = tk1 + r / TC_TCOL, k2 = tk2 + r % TC_TCOL;
     const bool inside = k1 < N && k2 < N;
-    float acc[64];
+    const float f1 = (float)(r / TC_TCOL), f2 = (float)(r % TC_TCOL);  // pixel offset in the tile
+    float acc[64];  // this group's accumulator columns [64 grp, 64 grp + 64) of pixel r
 #pragma unroll
     for (int j = 0; j < 64; ++j) acc[j] = 0.f;
     const uint32_t tlane = (uint32_t)((warp & 3) * 32) << 16;
-    auto flush = [&](int jf) {  // add TMEM block jf (columns [64 h, 64 h + 64) of lane r) into acc
+    auto flush = [&](int jf) {  // add TMEM block jf (columns [64 grp, 64 grp + 64) of lane r) into acc
       const int buf = jf & 1;
       mbar_wait(acc_full + 8 * buf, (uint32_t)((jf >> 1) & 1), 6, jf);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t v[32];
-        tmem_ld32(tmem + tlane + (uint32_t)(buf * TC_N + 64 * h + 32 * c), v);
+        tmem_ld32(tmem + tlane + (uint32_t)(buf * TC_N + 64 * grp + 32 * c), v);
 #pragma unroll
         for (int j = 0; j < 32; ++j) acc[32 * c + j] += __uint_as_float(v[j]);
       }
@@ -259,35 +283,35 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
       mbar_arrive(acc_empty + 8 * buf);
     };
     int next_flush = 0;
-    for (int a = 0; a < n_angles; ++a) {
-      const int s = a % TC_NS;
-      const uint32_t par = (uint32_t)((a / TC_NS) & 1);
-      const uint32_t st = sm + s * TC_STAGE;
-      const uint32_t whi = st, wlo = st + TC_OPB, tab = st + 4 * TC_OPB;
-      mbar_wait(full_g + 8 * s, par, 1, a);  // G tiles, basis table and BPAngle of angle a have landed
+    for (int a = grp; a < n_angles; a += 2) {
+      const int ts = a % TC_NT, ws = a % TC_NW;
+      const uint32_t tab = sm + TC_TOFF + ts * TC_TSLOT;
+      const uint32_t whi = sm + TC_WOFF + ws * 2 * TC_OPB, wlo = whi + TC_OPB;
+      mbar_wait(full_t + 8 * ts, (uint32_t)((a / TC_NT) & 1), 1, a);  // basis table and BPAngle of angle a
       const size_t aoff = (size_t)((uintptr_t)(ang + a) & 15);  // the staged copy starts 16-byte aligned
-      const BPAngle &A = *reinterpret_cast<const BPAngle *>(smg + s * TC_STAGE + 4 * TC_OPB + TC_TABB + aoff);
-      const int m_lo = tc_window(A.u0, A.du1, A.du2, A.imin, tk1, tk2);
-      const double u = fma(A.du1, (double)k1, fma(A.du2, (double)k2, A.u0));
-      const double cu = floor(u);
-      const float ph = (float)(u - cu);
-      const int P = A.P, S = A.S;
+      const BPAngle &A = *reinterpret_cast<const BPAngle *>(smg + TC_TOFF + ts * TC_TSLOT + TC_TABB + aoff);
+      // locate: the tile origin in FP64 (uniform), the pixel's offset (|.| < 24 cells) in FP32, as K4 v3
+      const double ut = fma(A.du1, (double)tk1, fma(A.du2, (double)tk2, A.u0));
+      const double umin = ut + fmin(0.0, A.du1 * (TC_TR - 1)) + fmin(0.0, A.du2 * (TC_TCOL - 1));
+      const int m_lo = ((((int)floor(umin)) - 1 + A.imin + HCv) & ~3) - HCv;
+      const double ct = floor(ut);
+      const float w0 = (float)(ut - ct) + fmaf((float)A.du1, f1, (float)A.du2 * f2);
+      const float cf = floorf(w0);
+      const float ph = w0 - cf;
+      const int P = A.P;
       int p = 0;
-      for (int k = 1; k < P; ++k) p += ph >= (float)A.bp[k] ? 1 : 0;
-      const float tau = ph - (float)A.bp[p];
-      const int o = (int)cu + A.imin - m_lo;  // window position of sample i = 0
-      const int ilo = A.ilo[p], ihi = min((int)A.ihi[p], S - 1);
-      // zero this thread's half of the pixel's W_hi / W_lo rows, then its weights
 #pragma unroll
-      for (int q = 4 * h; q < 4 * h + 4; ++q) {  // logical chunk q of the row sits at chunk q ^ (r & 7)
-        st_shared_v4z(whi + r * TC_ROWB + ((q ^ (r & 7)) << 4));
-        st_shared_v4z(wlo + r * TC_ROWB + ((q ^ (r & 7)) << 4));
-      }
-      if (inside) {
-        const uint32_t bp = tab + (uint32_t)(p * BP_SMAX * 8 * 4);
-        for (int i = ilo; i <= ihi; ++i) {
-          const int pos = o + i;
-          if ((pos >> 4) != h) continue;  // the other half-row thread owns this position
+      for (int k = 1; k < BP_PMAX; ++k) p += (k < P && ph >= A.bpf[k]) ? 1 : 0;
+      const float tau = ph - A.bpf[p];
+      const int o = (int)ct + (int)cf + A.imin - m_lo;  // window position of sample i = 0
+      const int ilo = A.ilo[p], ihi = min((int)A.ihi[p], A.S - 1);
+      float wv[8];
+      const uint32_t bp = tab + (uint32_t)(p * TC_PSTR);
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const int i = ilo + q;
+        wv[q] = 0.f;
+        if (i <= ihi) {
           const float4 c03 = ld_shared_v4(bp + i * 32), c47 = ld_shared_v4(bp + i * 32 + 16);
           float w = c47.y;
           w = fmaf(w, tau, c47.x);
@@ -295,68 +319,87 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
           w = fmaf(w, tau, c03.z);
           w = fmaf(w, tau, c03.y);
           w = fmaf(w, tau, c03.x);
-          const uint32_t off = sw128(r, pos);
-          st_shared_f32(whi + off, w);
-          st_shared_f32(wlo + off, tf32_lo(w));
+          wv[q] = inside ? w : 0.f;
         }
       }
+      mbar_arrive(t_empty + 8 * ts);  // done with the tables of this slot
+      mbar_wait(w_empty + 8 * ws, (uint32_t)(((a / TC_NW) & 1) ^ 1), 8, a);  // the MMAs of angle a - NW are done
+      // the pixel's W_hi / W_lo rows: zero, then the weights at window positions o + ilo + q
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {  // chunk q ^ (r & 7): the 8 lanes of a quarter warp hit distinct banks
+        st_shared_v4z(whi + r * TC_ROWB + ((q ^ (r & 7)) << 4));
+        st_shared_v4z(wlo + r * TC_ROWB + ((q ^ (r & 7)) << 4));
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q)
+        if (ilo + q <= ihi) {
+          const uint32_t off = sw128(r, o + ilo + q);
+          st_shared_f32(whi + off, wv[q]);
+          st_shared_f32(wlo + off, tf32_lo(wv[q]));
+        }
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> async proxy (MMA)
-      mbar_arrive(full_w + 8 * s);
-      // block jf is flushed once block jf + 1 is fully produced (its MMAs are then long done)
-      while (next_flush + 2 <= (a + 1) / TC_F) flush(next_flush++);
+      mbar_arrive(full_w + 8 * ws);
+      // block jf is flushed once this group has produced its angles of block jf + 1 (their MMAs wait
+      // for W only a few angles behind, so block jf's MMAs are done)
+      while (next_flush + 2 <= (a + 2) / TC_F) flush(next_flush++);
     }
     while (next_flush < nblk) flush(next_flush++);
     // ---------------------------------------------------------------- epilogue: acc -> b[:, k1, k2]
     if (inside) {
 #pragma unroll
       for (int j = 0; j < 64; ++j) {
-        const int b = b0 + 64 * h + j;
+        const int b = b0 + 64 * grp + j;
         if (b < B) out[((size_t)b * N + k1) * N + k2] = scale * acc[j];
       }
     }
   } else if (warp == 8) {
-    // ---------------------------------------------------------------- TMA producer
+    // ---------------------------------------------------------------- TMA producer (tables ahead, then G)
     if (lane == 0) {
-      // this angle's window and sub-interval count from its BPAngle (global, prefetched one angle ahead)
-      double u0 = ang[0].u0, du1 = ang[0].du1, du2 = ang[0].du2;
-      int imin = ang[0].imin, P = ang[0].P;
-      for (int a = 0; a < n_angles; ++a) {
-        const int s = a % TC_NS;
-        const uint32_t par = (uint32_t)((a / TC_NS) & 1);
-        const int m_lo = tc_window(u0, du1, du2, imin, tk1, tk2);
-        const uint32_t tab_bytes = (uint32_t)(P * BP_SMAX * 8 * 4);  // rows of the P sub-intervals only
-        if (a + 1 < n_angles) {
-          u0 = ang[a + 1].u0;
-          du1 = ang[a + 1].du1;
-          du2 = ang[a + 1].du2;
-          imin = ang[a + 1].imin;
-          P = ang[a + 1].P;
-        }
-        mbar_wait(empty + 8 * s, par ^ 1, 2, a);
-        const uint32_t st = sm + s * TC_STAGE;
+      int at = 0;  // next angle whose tables are issued (runs up to NT - 1 angles ahead of the G loads)
+      auto issue_tables = [&](int a) {
+        const int ts = a % TC_NT;
+        mbar_wait(t_empty + 8 * ts, (uint32_t)(((a / TC_NT) & 1) ^ 1), 9, a);
+        const uint32_t tab = sm + TC_TOFF + ts * TC_TSLOT;
         const char *asrc = reinterpret_cast<const char *>(ang + a);
         const char *aal = reinterpret_cast<const char *>((uintptr_t)asrc & ~(uintptr_t)15);
-        mbar_expect_tx(full_g + 8 * s, 2 * TC_OPB + tab_bytes + TC_ANGB);
-        bulk_g2s(st + 4 * TC_OPB, Btab + (size_t)a * BP_PMAX * BP_SMAX * 8, tab_bytes, full_g + 8 * s);
-        bulk_g2s(st + 4 * TC_OPB + TC_TABB, aal, TC_ANGB, full_g + 8 * s);
+        mbar_expect_tx(full_t + 8 * ts, (uint32_t)(maxP * BP_SMAX * 32 + TC_ANGB));
+        const float *src = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
+        for (int q = 0; q < maxP; ++q)  // per-sub-interval rows into padded slots (no global read first)
+          bulk_g2s(tab + q * TC_PSTR, src + q * BP_SMAX * 8, BP_SMAX * 32, full_t + 8 * ts);
+        bulk_g2s(tab + TC_TABB, aal, TC_ANGB, full_t + 8 * ts);
+      };
+      for (int a = 0; a < n_angles; ++a) {
+        while (at < n_angles && at < a + TC_NT - 1) issue_tables(at++);
+        const int gs = a % TC_NG, ts = a % TC_NT;
+        // the window from the staged BPAngle record (landed NT - 2 angles ago): no global load here
+        mbar_wait(full_t + 8 * ts, (uint32_t)((a / TC_NT) & 1), 10, a);
+        const size_t aoff = (size_t)((uintptr_t)(ang + a) & 15);
+        const BPAngle &A = *reinterpret_cast<const BPAngle *>(smg + TC_TOFF + ts * TC_TSLOT + TC_TABB + aoff);
+        const int m_lo = tc_window(A.u0, A.du1, A.du2, A.imin, tk1, tk2);
+        mbar_wait(g_empty + 8 * gs, (uint32_t)(((a / TC_NG) & 1) ^ 1), 2, a);
+        TC_TR_MARK(7, a);
+        const uint32_t g = sm + TC_GOFF + gs * 2 * TC_OPB;
+        mbar_expect_tx(full_g + 8 * gs, 2 * TC_OPB);
         // sample m <-> column m + HC of the corrected rows; outside the rows / batch: zero fill
-        tma_load_3d(st + 2 * TC_OPB, &map_g, m_lo + HCv, a, b0, full_g + 8 * s);
-        tma_load_3d(st + 3 * TC_OPB, &map_lo, m_lo + HCv, a, b0, full_g + 8 * s);
+        tma_load_3d(g, &map_g, m_lo + HCv, a, b0, full_g + 8 * gs);
+        tma_load_3d(g + TC_OPB, &map_lo, m_lo + HCv, a, b0, full_g + 8 * gs);
       }
     }
   } else {
     // ---------------------------------------------------------------- MMA issuer (one thread)
     if (lane == 0) {
       for (int a = 0; a < n_angles; ++a) {
-        const int s = a % TC_NS;
-        const uint32_t par = (uint32_t)((a / TC_NS) & 1);
+        const int ws = a % TC_NW, gs = a % TC_NG;
         const int j = a / TC_F, buf = j & 1;
         const bool first = a % TC_F == 0, last = a % TC_F == TC_F - 1 || a == n_angles - 1;
         if (first && j >= 2) mbar_wait(acc_empty + 8 * buf, (uint32_t)(((j - 2) >> 1) & 1), 7, a);
-        mbar_wait(full_w + 8 * s, par, 3, a);  // implies full_g (the producers waited on it)
+        mbar_wait(full_g + 8 * gs, (uint32_t)((a / TC_NG) & 1), 4, a);
+        TC_TR_MARK(5, a);
+        mbar_wait(full_w + 8 * ws, (uint32_t)((a / TC_NW) & 1), 3, a);
+        TC_TR_MARK(6, a);
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t st = sm + s * TC_STAGE;
-        const uint32_t whi = st, wlo = st + TC_OPB, ghi = st + 2 * TC_OPB, glo = st + 3 * TC_OPB;
+        const uint32_t whi = sm + TC_WOFF + ws * 2 * TC_OPB, wlo = whi + TC_OPB;
+        const uint32_t ghi = sm + TC_GOFF + gs * 2 * TC_OPB, glo = ghi + TC_OPB;
         const uint32_t As[3] = {whi, whi, wlo}, Bs[3] = {ghi, glo, ghi};
         const uint32_t d = tmem + (uint32_t)(buf * TC_N);
 #pragma unroll
@@ -365,7 +408,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
           for (int kk = 0; kk < TC_K / 8; ++kk)  // K = 8 TF32 (32 bytes) per instruction
             umma_tf32(d, umma_desc(As[pr] + 32 * kk), umma_desc(Bs[pr] + 32 * kk),
                       (!first || pr > 0 || kk > 0) ? 1u : 0u);
-        umma_commit(empty + 8 * s);  // the stage is free once these MMAs have read it
+        umma_commit(w_empty + 8 * ws);  // the W and G slots are free once these MMAs have read them
+        umma_commit(g_empty + 8 * gs);
         if (last) umma_commit(acc_full + 8 * buf);  // block j complete in TMEM buffer j & 1
       }
     }
@@ -424,14 +468,15 @@ bool bp_tc_supported(int n, const double *angles, double lx, double ly, double z
     const double H = 0.5 * (lx * (c + s) + zeta + 3.0 * ly);  // >= the half support of C_t
     const int cw = (int)std::ceil(H / ly - 1e-12);
     if ((int)std::ceil(span) + 2 + 3 + (2 * cw + 1) > TC_K) return false;  // + 3: aligned window start
+    if (2 * cw + 1 > 8) return false;  // a producer thread holds at most 8 weights of its pixel
   }
   return true;
 }
 
-size_t bp_tc_smem() { return (size_t)TC_NS * TC_STAGE + 24 * TC_NS + 64 + 1024; }
+size_t bp_tc_smem() { return (size_t)TC_BOFF + 8 * (2 * TC_NT + 2 * TC_NW + 2 * TC_NG + 4) + 16 + 1024; }
 
 cudaError_t backproject_tc(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
-                           const float *gt_lo, int ldt, float *out, double scale, cudaStream_t s) {
+                           const float *gt_lo, int ldt, float *out, double scale, int maxP, cudaStream_t s) {
   if (B <= 0) return cudaSuccess;
   CUtensorMap mg, ml;
   const int Mt = M + 2 * HCv;
@@ -441,7 +486,20 @@ cudaError_t backproject_tc(int N, int n_angles, int M, int B, const BPAngle *ang
   cudaError_t e = cudaFuncSetAttribute(bp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
   if (e != cudaSuccess) return e;
   dim3 grid((N + TC_TCOL - 1) / TC_TCOL, (N + TC_TR - 1) / TC_TR, (B + TC_N - 1) / TC_N);
-  bp_tc_kernel<<<grid, TC_THREADS, sm, s>>>(N, n_angles, B, ang, Btab, mg, ml, out, (float)scale);
+  bp_tc_kernel<<<grid, TC_THREADS, sm, s>>>(N, n_angles, B, ang, Btab, mg, ml, out, (float)scale, maxP);
+#ifdef BSCT_TC_TRACE
+  if (grid.z > 3 && grid.y > 20) {
+    static long long h[8][512];
+    cudaStreamSynchronize(s);
+    cudaMemcpyFromSymbol(h, g_tc_trace, sizeof(h));
+    const char *nm[8] = {"p:t_wait0", "p:t_got", "p:w_wait0", "p:w_got", "p:arrived", "m:g_got", "m:w_got", "tma:g_empty"};
+    for (int a = 100; a < 112; ++a) {
+      fprintf(stderr, "a=%d", a);
+      for (int k = 0; k < 8; ++k) fprintf(stderr, " %s=%lld", nm[k], h[k][a] - h[0][100]);
+      fprintf(stderr, "\n");
+    }
+  }
+#endif
   return cudaGetLastError();
 }
 

@@ -99,13 +99,14 @@ struct BPAngle {
   double bp[BP_PMAX];  // sub-interval starts in [0,1), bp[0] = 0, unused = +huge
   int P, S, imin, pad;
   unsigned char ilo[BP_PMAX], ihi[BP_PMAX];  // per sub-interval: first / last nonzero basis row
+  float bpf[BP_PMAX];                         // bp as FP32 (K4 v4's sub-interval search)
 };
 // K4 v4 (bp_tc.cu): tensor-core back projection of g~ = gt + gt_lo (TF32 split by K3; row stride ldt,
 // a multiple of 4 floats for TMA); bp_tc_supported: every 8 x 16 pixel tile fits the 32-sample window
 bool bp_tc_supported(int n, const double *angles, double lx, double ly, double zeta);
 size_t bp_tc_smem();
 cudaError_t backproject_tc(int N, int n_angles, int M, int B, const BPAngle *ang, const float *Btab, const float *gt,
-                           const float *gt_lo, int ldt, float *out, double scale, cudaStream_t s);
+                           const float *gt_lo, int ldt, float *out, double scale, int maxP, cudaStream_t s);
 size_t bp_table_floats(int n);  // size of the basis table B[n][BP_PMAX][BP_SMAX][8]
 int bp_v2_max_cells(double lx, double ly, double zeta);  // 0: geometry not supported by v2
 int bp_v2_max_p(int n, const double *angles, double lx, double ly, double zeta);  // host, sub-intervals per cell

@@ -223,3 +223,31 @@ def test_two_devices_one_process(cuda_lib):
             outs.append((taps.cpu(), b.cpu()))
     for t, b in outs[1:]:
         assert torch.equal(t, outs[0][0]) and torch.equal(b, outs[0][1])
+
+
+@pytest.mark.parametrize("N,n,M,zeta,lx,B", [(512, 360, 725, 1.0, 1.0, 130), (100, 60, 151, 1.0, 1.0, 3),
+                                             (257, 90, 401, 1.5, 1.0, 5), (64, 32, 101, 0.0, 1.0, 2),
+                                             (129, 45, 181, 1.0, 0.8, 129), (33, 30, 51, 1.0, 1.0, 1)])
+def test_bp_tensor_core_equals_cuda_core(cuda_lib, N, n, M, zeta, lx, B, monkeypatch):
+    """K4 v4 (tcgen05 tensor cores, 3xTF32, bp_tc.cu) against K4 v3 (FP32 CUDA cores) on the same
+    sinograms: ragged pixel tiles (N not a multiple of 8 / 16), slice counts around the 128-slice
+    MMA width, lambda_x != 1, no blur; and sampled pixels against the FP64 oracle."""
+    import torch
+    rng = np.random.default_rng(N + B)
+    ang = np.arange(n) * np.pi / n + 0.013
+    g = dict(N=N, lambda_x=lx, angles=ang, lambda_y=1.0, n_det=M, zeta=zeta)
+    sino = rng.uniform(-1, 1, (B, n, M))
+    sd = to_dev(sino, "f32")
+    taps = torch.zeros((2 * N - 1, 2 * N - 1), device="cuda")
+    taps[N - 1, N - 1] = 1.0  # the back projection does not read the filter
+    out = {}
+    for v3 in ("0", "1"):
+        monkeypatch.setenv("BSCT_BP_V3", v3)
+        plan = cuda_lib.plan_create(g, taps, max_batch=B)
+        b = torch.empty((B, N, N), device="cuda")
+        cuda_lib.backproject(plan, sd, b)
+        torch.cuda.synchronize()
+        out[v3] = to_np(b)
+    assert rel_l2(out["0"], out["1"]) < 5e-6
+    k1, k2 = rng.integers(0, N, 80), rng.integers(0, N, 80)
+    assert rel_l2(out["0"][B - 1][k1, k2], backproject(g, sino[B - 1], pixels=(k1, k2))) < 1e-5
