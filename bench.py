@@ -65,8 +65,9 @@ def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
         d = json.load(open(p))
-        return dict(hbm_gbs=float(d["hbm_gbs"]), source="measured", sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)))
-    return dict(hbm_gbs=6650.0, source="fallback", sm_max_mhz=1965.0)
+        return dict(hbm_gbs=float(d["hbm_gbs"]), source="measured", sm_max_mhz=float(d.get("sm_max_mhz", 1965.0)),
+                    bf16_tflops=float(d.get("bf16_tflops", 1590.0)))
+    return dict(hbm_gbs=6650.0, source="fallback", sm_max_mhz=1965.0, bf16_tflops=1590.0)
 
 
 def ncu_traffic(kernel: str, slices: int):
@@ -74,13 +75,11 @@ def ncu_traffic(kernel: str, slices: int):
     (profiles/*/ncu_traffic.json, bytes per slice x slices of this launch), else None."""
     import glob
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*", "ncu_traffic.json")))
-    if not files:
-        return None, None
-    d = json.load(open(files[-1]))
-    k = d["kernels"].get(kernel)
-    if not k:
-        return None, None
-    return k["bytes_per_slice"] * slices, os.path.relpath(files[-1], ROOT)
+    for f in reversed(files):  # the newest capture of this kernel
+        k = json.load(open(f))["kernels"].get(kernel)
+        if k:
+            return k["bytes_per_slice"] * slices, os.path.relpath(f, ROOT)
+    return None, None
 
 
 def fp32_peak_tflops(sm_mhz: float, sms: int = 148) -> float:
@@ -363,6 +362,21 @@ def fma_peak():
     return fp32_peak_tflops(1965.0), "derived: 148 SMs x 128 FP32 lanes x 2 x 1965 MHz (B200_PROFILING.md)"
 
 
+def bp_tensor_core_path(cfg) -> bool:
+    """Whether the library takes K4 v4 (tensor cores) for this geometry: the host check of
+    bp_tc.cu (every 8 x 16 pixel tile's samples fit the 32-sample window, <= 8 samples per pixel)."""
+    if cfg.dtype != "f32" or os.environ.get("BSCT_BP_V3") == "1":
+        return False
+    lx, ly, z = cfg.lambda_x, cfg.lambda_y, cfg.zeta
+    for t in np.asarray(cfg.angles, dtype=np.float64):
+        c, s_ = abs(np.cos(t)), abs(np.sin(t))
+        span = (lx / ly) * (7 * s_ + 15 * c)
+        cw = int(np.ceil(0.5 * (lx * (c + s_) + z + 3 * ly) / ly - 1e-12))
+        if int(np.ceil(span)) + 5 + 2 * cw + 1 > 32 or 2 * cw + 1 > 8:
+            return False
+    return True
+
+
 def roofline(per: dict, cfg, B: int, clk: dict, peaks: dict):
     """Roofline of the dominant kernel class of one profiled step (library CUDA events around every
     launch on its stream) and the HBM rooflines of the three FFT passes / whole CG iteration."""
@@ -393,32 +407,65 @@ def roofline(per: dict, cfg, B: int, clk: dict, peaks: dict):
                                    "state_floor_bytes": B * 24 * N * N,
                                    "frac_state_floor": B * 24 * N * N / (it_ms / 1e3) / 1e9 / peaks["hbm_gbs"],
                                    "note": "north_star: FFT normal-operator apply >= 60% of HBM roofline"}
-    if dom == "backproject":
+    rooflines = {}
+    peak_fp32, fp32_src = fma_peak()
+    if "backproject" in per and per["backproject"][1] > 0:
+        ms_launch = per["backproject"][0] / per["backproject"][1]
         # algorithmic FLOP per vox-angle (K4): S_eff samples x (degree-5 Horner = 5 FMA
         # + 1 FMA accumulate) x 2 flop + 2 FMA for k_theta; S_eff = mean support / lambda_y
         w_mean = (4 / np.pi) * cfg.lambda_x + cfg.zeta + 3 * cfg.lambda_y
         flops = vox_angles * (w_mean / cfg.lambda_y * 12.0 + 4.0)
-        ms_launch = per[dom][0] / max(per[dom][1], 1)
         ach = flops / (ms_launch / 1e3) / 1e12
-        peak, peak_src = fma_peak()
-        tb, tsrc = ncu_traffic("bp_v3_kernel", B)
-        roof = {"kernel": "backproject (K4)", "bound": "alu", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": tb, "traffic_source": tsrc,
-                "algorithmic_bytes": B * 4 * (n_ang * (M + 50) + N * N),
-                "peak_source": peak_src,
-                "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6); "
-                        "K4 evaluates it from per-tile tables and is shared-memory bound"}
-    else:
-        # HBM-bound FFT passes: compulsory bytes of the pass per launch (K5)
-        byts = cg_bytes.get(dom, 0)
-        ms_launch = per[dom][0] / max(per[dom][1], 1)
-        ach = byts / (ms_launch / 1e3) / 1e9
-        kname = {"pass_a": "cg_pass_a_1024_kernel", "pass_b": "pass_b_1024_kernel",
-                 "pass_c": "cg_pass_c_1024_kernel"}.get(dom, dom)
-        tb, tsrc = ncu_traffic(kname, B)
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                "frac": ach / peaks["hbm_gbs"], "traffic": tb, "traffic_source": tsrc,
-                "peak_source": peaks["source"]}
+        tc = bp_tensor_core_path(cfg)
+        if tc:
+            # K4 v4 (bp_tc.cu): executed tcgen05 work = per (128-pixel tile, 128-slice group, angle)
+            # 12 MMAs of 128 x 128 x 8 TF32 (3xTF32 split, K = 32 window); peak = measured bf16 burst
+            # x the nominal TF32 / BF16 ratio (1.1 / 2.25 PFLOP/s dense, B200_PROFILING.md)
+            tiles = -(-N // 16) * -(-N // 8) * -(-B // 128)
+            mma_flops = tiles * n_ang * 12 * 2.0 * 128 * 128 * 8
+            tf32_peak = peaks["bf16_tflops"] * 1.1 / 2.25
+            tb, tsrc = ncu_traffic("bp_tc_kernel", B)
+            rooflines["backproject"] = {
+                "kernel": "backproject (K4 v4, tcgen05 kind::tf32)", "bound": "tensor", "traffic": tb,
+                "traffic_source": tsrc,
+                "achieved": mma_flops / (ms_launch / 1e3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": mma_flops / (ms_launch / 1e3) / 1e12 / tf32_peak,
+                "peak_source": "derived: MEASURED_PEAKS.json bf16_tflops x 1.1/2.25 (nominal TF32/BF16 dense)",
+                "ms_per_launch": ms_launch, "algorithmic_tflops": ach,
+                "algorithmic_frac_of_fp32_peak": ach / peak_fp32,
+                "note": "achieved = executed MMA FLOP (3 TF32 products on the zero-padded 32-sample window); "
+                        "algorithmic_tflops = the direct closed-form FLOP (12 S_eff + 4 per vox-angle) / time"}
+        else:
+            tb, tsrc = ncu_traffic("bp_v3_kernel", B)
+            rooflines["backproject"] = {
+                "kernel": "backproject (K4 v3)", "bound": "alu", "achieved": ach, "peak": peak_fp32,
+                "unit": "TFLOP/s", "frac": ach / peak_fp32, "traffic": tb, "traffic_source": tsrc,
+                "peak_source": fp32_src, "ms_per_launch": ms_launch,
+                "note": "FLOP = the direct closed-form evaluation (12 S_eff + 4 per vox-angle, DESIGN.md 6)"}
+    if "pass_b" in per and per["pass_b"][1] > 0:
+        # pass B: forward + inverse column FFTs of length L on Q columns per slice (nominal
+        # 5 L log2 L flops each), bound by the FP32 pipe (ncu: FMA pipe ~70%); HBM fraction beside it
+        ms_launch = per["pass_b"][0] / per["pass_b"][1]
+        fft_flops = B * Q * 2 * 5.0 * L * np.log2(L)
+        ach = fft_flops / (ms_launch / 1e3) / 1e12
+        tb, tsrc = ncu_traffic("pass_b_1024_kernel", B)
+        rooflines["pass_b"] = {"kernel": "pass_b (column FFT x spectrum x inverse FFT)", "bound": "alu",
+                               "achieved": ach, "peak": peak_fp32, "unit": "TFLOP/s", "frac": ach / peak_fp32,
+                               "peak_source": fp32_src, "ms_per_launch": ms_launch,
+                               "hbm_frac": kernels["pass_b"]["frac_of_measured_hbm"] if "pass_b" in kernels else None,
+                               "traffic": tb, "traffic_source": tsrc,
+                               "note": "FLOP = 2 x 5 L log2 L per column (nominal radix-2 count); the FP32 "
+                                       "FMA peak is the same for FFMA and FFMA2 (profiles/r02/fma_peak.json)"}
+    for kk, kname in (("pass_a", "cg_pass_a_1024_kernel"), ("pass_c", "cg_pass_c_1024_kernel")):
+        if kk in kernels:
+            tb, tsrc = ncu_traffic(kname, B)
+            rooflines[kk] = {"kernel": kk, "bound": "hbm", "achieved": kernels[kk]["achieved_gbs"],
+                             "peak": peaks["hbm_gbs"], "unit": "GB/s", "frac": kernels[kk]["frac_of_measured_hbm"],
+                             "traffic": tb, "traffic_source": tsrc, "peak_source": peaks["source"],
+                             "ms_per_launch": kernels[kk]["ms_per_launch"]}
+    roof = dict(rooflines.get(dom) or next(iter(rooflines.values())))
+    roof["dominant_class"] = dom
+    roof["all"] = rooflines
     return roof, kernels
 
 

@@ -1,4 +1,6 @@
-timeout 1200 python -m pytest tests/test_gpu_backproject.py tests/test_gpu_fullsize.py tests/test_gpu_lambda_x.py tests/test_gpu_race_stress.py tests/test_gpu_determinism.py tests/test_gpu_solvers.py -q -x 2>&1 | tail -3
-python tools/check_bp_tc.py 128 > gpurun_out/chk.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:bp_tc_kernel -s 1 -c 1 -o gpurun_out/bptc5 python tools/check_bp_tc.py 128 > gpurun_out/chk_ncu.log 2>&1
-echo rc=$?
+timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-cufft --json-out gpurun_out/bench_v2.json > gpurun_out/bench_v2.log 2>&1; echo rc=$?
+python -c "
+import json; d=json.load(open('gpurun_out/bench_v2.json'))
+print(d['value'], d['ms_per_step'], d['phases_ms'], d['kernel_ms_per_step'], d['e2e']['value'], json.dumps(d['roofline'])[:300])"
+for ov in 1; do BSCT_PIPE_OVERLAP=$ov BSCT_PIPE_CHUNK=256 timeout 600 python bench.py --steps 3 --warmup 3 --no-cpu --no-cufft --no-e2e > gpurun_out/bench_ov.log 2>&1; tail -c 300 gpurun_out/bench_ov.log | head -c 0; python -c "
+import json; d=json.loads(open('gpurun_out/bench_ov.log').read().strip().splitlines()[-1]); print('overlap', d['value'], d['ms_per_step'])"; done
