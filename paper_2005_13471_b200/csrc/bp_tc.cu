@@ -46,7 +46,7 @@ namespace {
 
 constexpr int TC_M = 128, TC_N = 128, TC_K = 32;  // pixels, slices, samples per angle
 constexpr int TC_TR = 8, TC_TCOL = 16;             // pixel tile: 8 rows x 16 columns
-constexpr int TC_THREADS = 320;  // 8 W-producer warps, TMA warp, MMA warp
+constexpr int TC_THREADS = 352;  // 8 W-producer warps, G TMA warp, MMA warp, table warp
 constexpr int TC_ROWB = 128;                        // bytes per operand row (32 x FP32)
 constexpr int TC_OPB = TC_M * TC_ROWB;              // one operand tile: 16 KB
 constexpr int HCv = 25;                             // correction filter half-width (R8)
@@ -137,10 +137,11 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map
 //   W       TC_NW slots of W_hi, W_lo (16 KB each); released by the MMAs (w_empty).
 //   G       TC_NG slots of G_hi, G_lo (16 KB each), TMA; released by the MMAs (g_empty).
 constexpr int TC_PSTR = BP_SMAX * 8 * 4 + 16;                 // bytes per sub-interval in smem
-constexpr int TC_TABB = BP_PMAX * TC_PSTR;                     // basis table slot
+constexpr int TC_PMAXT = 10;                                   // sub-intervals per angle (host-checked)
+constexpr int TC_TABB = TC_PMAXT * TC_PSTR;                    // basis table slot
 constexpr int TC_ANGB = (int)((sizeof(BPAngle) + 8 + 15) & ~(size_t)15);  // BPAngle + up to 8 B misalignment
 constexpr int TC_TSLOT = (TC_TABB + TC_ANGB + 127) & ~127;
-constexpr int TC_NT = 4, TC_NW = 3, TC_NG = 3;
+constexpr int TC_NT = 5, TC_NW = 3, TC_NG = 3;
 constexpr int TC_WOFF = 0, TC_GOFF = TC_NW * 2 * TC_OPB, TC_TOFF = TC_GOFF + TC_NG * 2 * TC_OPB;
 constexpr int TC_BOFF = (TC_TOFF + TC_NT * TC_TSLOT + 127) & ~127;  // barriers
 constexpr int TC_PROD = 256;  // producer threads: pixel t & 127, row half t >> 7
@@ -230,7 +231,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
   if (threadIdx.x == 0) {
     for (int s = 0; s < TC_NT; ++s) {
       mbar_init(full_t + 8 * s, 1);
-      mbar_init(t_empty + 8 * s, TC_PROD / 2);
+      mbar_init(t_empty + 8 * s, TC_PROD / 2 + 1);  // the angle's producer group + the G warp
     }
     for (int s = 0; s < TC_NW; ++s) {
       mbar_init(full_w + 8 * s, TC_PROD / 2);
@@ -352,11 +353,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
         if (b < B) out[((size_t)b * N + k1) * N + k2] = scale * acc[j];
       }
     }
-  } else if (warp == 8) {
-    // ---------------------------------------------------------------- TMA producer (tables ahead, then G)
+  } else if (warp == 10) {
+    // ---------------------------------------------------------------- table producer (bulk copies, NT - 1 ahead)
     if (lane == 0) {
-      int at = 0;  // next angle whose tables are issued (runs up to NT - 1 angles ahead of the G loads)
-      auto issue_tables = [&](int a) {
+      for (int a = 0; a < n_angles; ++a) {
         const int ts = a % TC_NT;
         mbar_wait(t_empty + 8 * ts, (uint32_t)(((a / TC_NT) & 1) ^ 1), 9, a);
         const uint32_t tab = sm + TC_TOFF + ts * TC_TSLOT;
@@ -364,20 +364,23 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
         const char *aal = reinterpret_cast<const char *>((uintptr_t)asrc & ~(uintptr_t)15);
         mbar_expect_tx(full_t + 8 * ts, (uint32_t)(maxP * BP_SMAX * 32 + TC_ANGB));
         const float *src = Btab + (size_t)a * BP_PMAX * BP_SMAX * 8;
-        for (int q = 0; q < maxP; ++q)  // per-sub-interval rows into padded slots (no global read first)
+        for (int q = 0; q < maxP; ++q)  // per-sub-interval rows into padded slots
           bulk_g2s(tab + q * TC_PSTR, src + q * BP_SMAX * 8, BP_SMAX * 32, full_t + 8 * ts);
         bulk_g2s(tab + TC_TABB, aal, TC_ANGB, full_t + 8 * ts);
-      };
+      }
+    }
+  } else if (warp == 8) {
+    // ---------------------------------------------------------------- G producer (TMA)
+    if (lane == 0) {
       for (int a = 0; a < n_angles; ++a) {
-        while (at < n_angles && at < a + TC_NT - 1) issue_tables(at++);
         const int gs = a % TC_NG, ts = a % TC_NT;
-        // the window from the staged BPAngle record (landed NT - 2 angles ago): no global load here
+        // the window from the staged BPAngle record (the table warp runs ahead): no global load here
         mbar_wait(full_t + 8 * ts, (uint32_t)((a / TC_NT) & 1), 10, a);
         const size_t aoff = (size_t)((uintptr_t)(ang + a) & 15);
         const BPAngle &A = *reinterpret_cast<const BPAngle *>(smg + TC_TOFF + ts * TC_TSLOT + TC_TABB + aoff);
         const int m_lo = tc_window(A.u0, A.du1, A.du2, A.imin, tk1, tk2);
+        mbar_arrive(t_empty + 8 * ts);  // done with this table slot
         mbar_wait(g_empty + 8 * gs, (uint32_t)(((a / TC_NG) & 1) ^ 1), 2, a);
-        TC_TR_MARK(7, a);
         const uint32_t g = sm + TC_GOFF + gs * 2 * TC_OPB;
         mbar_expect_tx(full_g + 8 * gs, 2 * TC_OPB);
         // sample m <-> column m + HC of the corrected rows; outside the rows / batch: zero fill
@@ -470,6 +473,7 @@ bool bp_tc_supported(int n, const double *angles, double lx, double ly, double z
     if ((int)std::ceil(span) + 2 + 3 + (2 * cw + 1) > TC_K) return false;  // + 3: aligned window start
     if (2 * cw + 1 > 8) return false;  // a producer thread holds at most 8 weights of its pixel
   }
+  if (bp_v2_max_p(n, angles, lx, ly, zeta) > TC_PMAXT) return false;  // table slots hold TC_PMAXT sub-intervals
   return true;
 }
 
