@@ -141,7 +141,7 @@ constexpr int TC_PMAXT = 10;                                   // sub-intervals 
 constexpr int TC_TABB = TC_PMAXT * TC_PSTR;                    // basis table slot
 constexpr int TC_ANGB = (int)((sizeof(BPAngle) + 8 + 15) & ~(size_t)15);  // BPAngle + up to 8 B misalignment
 constexpr int TC_TSLOT = (TC_TABB + TC_ANGB + 127) & ~127;
-constexpr int TC_NT = 5, TC_NW = 3, TC_NG = 3;
+constexpr int TC_NT = 5, TC_NW = 2, TC_NG = 4;  // W slot a % 2 = the producer group of angle a
 constexpr int TC_WOFF = 0, TC_GOFF = TC_NW * 2 * TC_OPB, TC_TOFF = TC_GOFF + TC_NG * 2 * TC_OPB;
 constexpr int TC_BOFF = (TC_TOFF + TC_NT * TC_TSLOT + 127) & ~127;  // barriers
 constexpr int TC_PROD = 256;  // producer threads: pixel t & 127, row half t >> 7
@@ -284,6 +284,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
       mbar_arrive(acc_empty + 8 * buf);
     };
     int next_flush = 0;
+    int pc = 0;  // first chunk of this thread's previous weights in its slot
+    {            // the slot starts as zero rows (no MMA has read it yet)
+      const uint32_t w0 = sm + TC_WOFF + grp * 2 * TC_OPB;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        st_shared_v4z(w0 + r * TC_ROWB + (q << 4));
+        st_shared_v4z(w0 + TC_OPB + r * TC_ROWB + (q << 4));
+      }
+    }
+    static_assert(TC_NW == 2, "the W slot of angle a must be owned by producer group a % 2");
     for (int a = grp; a < n_angles; a += 2) {
       const int ts = a % TC_NT, ws = a % TC_NW;
       const uint32_t tab = sm + TC_TOFF + ts * TC_TSLOT;
@@ -325,12 +335,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
       }
       mbar_arrive(t_empty + 8 * ts);  // done with the tables of this slot
       mbar_wait(w_empty + 8 * ws, (uint32_t)(((a / TC_NW) & 1) ^ 1), 8, a);  // the MMAs of angle a - NW are done
-      // the pixel's W_hi / W_lo rows: zero, then the weights at window positions o + ilo + q
+      // the pixel's W_hi / W_lo rows.  Slot ws = a % 2 = grp is only ever written by this thread
+      // (for this pixel): it holds the weights of angle a - 2 in chunks [pc, pc + 3) and zeros
+      // elsewhere, so clearing those three chunks restores a zero row; then the new weights at
+      // window positions o + ilo + q (program order: zero first)
 #pragma unroll
-      for (int q = 0; q < 8; ++q) {  // chunk q ^ (r & 7): the 8 lanes of a quarter warp hit distinct banks
-        st_shared_v4z(whi + r * TC_ROWB + ((q ^ (r & 7)) << 4));
-        st_shared_v4z(wlo + r * TC_ROWB + ((q ^ (r & 7)) << 4));
+      for (int q = 0; q < 3; ++q) {  // chunk c ^ (r & 7): the 8 lanes of a quarter warp hit distinct banks
+        const int c = min(pc + q, 7);
+        st_shared_v4z(whi + r * TC_ROWB + ((c ^ (r & 7)) << 4));
+        st_shared_v4z(wlo + r * TC_ROWB + ((c ^ (r & 7)) << 4));
       }
+      pc = (o + ilo) >> 2;  // <= 8 positions from here: <= 3 chunks
 #pragma unroll
       for (int q = 0; q < 8; ++q)
         if (ilo + q <= ihi) {
