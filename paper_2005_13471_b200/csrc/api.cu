@@ -112,6 +112,8 @@ struct bsct_plan_s {
   cudaStream_t cap = nullptr;                                  // graph capture of small solves
   std::vector<GraphEntry> graphs;
   std::vector<cudaEvent_t> pipe_ev;
+  std::vector<cudaStream_t> gstreams;  // streams of the chunked solver (BSCT_CHUNK_STREAMS)
+  std::vector<cudaEvent_t> gevents;
   // kernel-class profiler: CUDA events bracket every launch on the caller's stream
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_pool;
@@ -451,23 +453,44 @@ bsct_status backproject_t(bsct_plan p, const T *sino, T *b, int B, cudaStream_t 
   return BSCT_OK;
 }
 
-// Slices per solver chunk: the per-iteration working set of a chunk (x, r, p and the FFT
-// intermediate T1) is kept below an L2 budget (default 72 MB of the 126 MB L2;
-// BSCT_L2_BUDGET_MB overrides, BSCT_CG_CHUNK forces a chunk size, 0 = whole batch).
+// Slices per solver chunk.  Default for the FP32 L = 1024 warp passes (config 5): chunks of
+// SOLVE_CHUNK slices solved on SOLVE_STREAMS streams at once (chunk k on stream k % streams, all
+// its iterations back to back, the whole schedule captured into one CUDA graph): the 12 slices in
+// flight keep their x, r, p and T1 (61 MB) resident in the 126 MB L2, and the concurrent chunks fill
+// each other's kernel tails.  Measured on B200 (config 5, 2048 slices x 50 CG iterations, DIT
+// FFTs): 372 -> 325 ms (chunks of 2-4 on 3-6 streams within 2%; 1 stream or chunks >= 8 slower,
+// profiles/r02/chunks_v4.txt).  BSCT_CG_CHUNK forces a chunk size (0 = whole batch),
+// BSCT_L2_BUDGET_MB sizes chunks to an L2 budget, BSCT_CHUNK_STREAMS sets the streams.  The
+// kernel-class profiler (prof_on) always sees the plain whole-batch launches.
+constexpr int SOLVE_CHUNK = 3, SOLVE_STREAMS = 4;
+
+bool default_chunking(bsct_plan p, int B) {
+  return p->dt == BSCT_F32 && p->L == 1024 && !p->prof_on && B >= 8 * SOLVE_CHUNK && pass_c_warp_enabled() &&
+         pass_b_warp_enabled() && !p->solver_v1;
+}
+
 int solver_chunk(bsct_plan p, int B) {
   if (const char *e = getenv("BSCT_CG_CHUNK")) {
     const int c = atoi(e);
     return c <= 0 ? std::max(B, 1) : std::min(c, std::max(B, 1));
   }
-  // Measured on B200 (config 5): chunks of 6-24 slices were 1.3-2x slower than one
-  // whole-batch pass (the passes are issue/latency bound, and small grids add tails),
-  // so chunking is opt-in: BSCT_L2_BUDGET_MB enables it.
   double budget = 0.0;
   if (const char *e = getenv("BSCT_L2_BUDGET_MB")) budget = atof(e);
-  if (budget <= 0) return std::max(B, 1);
+  if (budget <= 0) return default_chunking(p, B) ? SOLVE_CHUNK : std::max(B, 1);
   const double per = (double)p->esize() * (3.0 * p->N * p->N + 2.0 * (p->L / 2 + 1) * p->N);
   const int c = (int)(budget * 1048576.0 / per);
   return std::max(1, std::min(c, std::max(B, 1)));
+}
+
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return (e && *e) ? atoi(e) : dflt;
+}
+
+// Streams of the chunked solve (chunk size cb < B): chunk k runs on stream k % ns
+int chunk_streams(bsct_plan p, int cb, int B) {
+  if (cb >= B) return 1;
+  return std::min(std::max(env_int("BSCT_CHUNK_STREAMS", default_chunking(p, B) ? SOLVE_STREAMS : 1), 1), 8);
 }
 
 template <typename T>
@@ -494,12 +517,18 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
     clear_graphs(p);  // captured graphs hold the old rho pointer
   }
   const char *ge = getenv("BSCT_GRAPH");
-  const bool graph = !(ge && ge[0] == '0') && !p->prof_on && (size_t)B * p->N * p->N <= ((size_t)1 << 22);
+  // chunked solves on several streams (L2-resident chunks) launch thousands of small kernels:
+  // captured as well, so that the host enqueue does not bound them
+  const int cb = solver_chunk(p, B);
+  const int ns = chunk_streams(p, cb, B);
+  const bool graph = !(ge && ge[0] == '0') && !p->prof_on &&
+                     ((size_t)B * p->N * p->N <= ((size_t)1 << 22) || ns > 1);
   if (!graph) return solve_launch_t<T>(p, b, x, B, iters, solver, resid, flags, s);
   // the key includes every switch that selects the launched code path
   const intptr_t path = (onchip_enabled() ? 1 : 0) | (pass_b_warp_enabled() ? 2 : 0) | (pass_c_warp_enabled() ? 4 : 0) |
                         (bulk_stage_enabled() ? 8 : 0) | (p->solver_v1 ? 16 : 0) |
-                        ((intptr_t)solver_chunk(p, B) << 8);
+                        ((intptr_t)cb << 8) | ((intptr_t)ns << 40) |
+                        ((getenv("BSCT_PASSC_TMA") && getenv("BSCT_PASSC_TMA")[0] == '1') ? 32 : 0);
   const void *key[8] = {b, x, (const void *)(intptr_t)B, (const void *)(intptr_t)iters,
                         (const void *)(intptr_t)solver, resid, flags, (const void *)path};
   for (auto &gk : p->graphs)
@@ -559,35 +588,83 @@ bsct_status solve_launch_t(bsct_plan p, const T *b, T *x, int B, int iters, int 
     auto *tw = (const cplx<T> *)p->tw;
     const int gparts = pass_b_blocks(p->L, p->dt == BSCT_F32);
     const size_t nn = (size_t)p->N * p->N;
-    for (int c0 = 0; c0 < B; c0 += cb) {
-      const int nb = std::min(cb, B - c0);
+    const size_t t1s = (size_t)(p->L / 2 + 1) * p->N;  // T1 entries per slice
+    // launch j (0: init, 1 + 3 it + {0, 1, 2}: passes A, B, C of iteration it, 3 iters + 1:
+    // final) of the chunk of nb slices from slice c0, on stream s; ws: workspaces at the chunk's
+    // own offsets (concurrent groups) or shared (sequential chunks)
+    const int nlaunch = 3 * iters + 2;
+    auto launch = [&](int c0, int nb, bool ws, int j, cudaStream_t s) -> bsct_status {
       const T *bc = b + c0 * nn;
       T *xc = x + c0 * nn;
+      T *rc = ws ? r + c0 * nn : r, *pc = ws ? pp + c0 * nn : pp;
+      cplx<T> *T1c = ws ? T1 + c0 * t1s : T1;
       FusedWork fw;
       fw.rho = p->rho + (size_t)c0 * (iters + 1);
       fw.rho_stride = iters + 1;
       fw.alpha = p->alpha + c0;
-      fw.gpart = p->gpart;
-      fw.rpart = p->rpart;
+      fw.gpart = ws ? p->gpart + (size_t)c0 * gparts : p->gpart;
+      fw.rpart = ws ? p->rpart + (size_t)2 * c0 * nparts : p->rpart;
       fw.nparts = nparts;
       fw.B = nb;
       fw.flags = (flags ? flags : p->flags) + c0;
       fw.resid = resid ? resid + (size_t)c0 * iters : nullptr;
       fw.iters = iters;
       fw.tau = p->tau;
-      LAUNCH(p, BSCT_K_SOLVER_INIT, 1,
-             (fused_init<T>(p->N, nb, bc, xc, r, solver == BSCT_CG ? pp : (T *)nullptr, fw, s)));
-      for (int it = 0; it < iters; ++it) {
-        if (solver == BSCT_CG)
-          LAUNCH(p, BSCT_K_PASS_A, 1, (fused_pass_a<T>(p->N, p->L, nb, it, xc, r, pp, T1, tw, fw, s)));
-        else
-          LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, nb, r, T1, tw, s)));
-        LAUNCH(p, BSCT_K_PASS_B, 1,
-               (pass_b<T>(p->N, p->L, nb, T1, (const T *)p->S, tw, solver == BSCT_LANDWEBER ? nullptr : p->gpart, s)));
-        LAUNCH(p, BSCT_K_PASS_C, 1, (fused_pass_c<T>(p->N, p->L, nb, it, solver, gparts, T1, xc, r, tw, fw, s)));
+      if (j == 0) {
+        LAUNCH(p, BSCT_K_SOLVER_INIT, 1,
+               (fused_init<T>(p->N, nb, bc, xc, rc, solver == BSCT_CG ? pc : (T *)nullptr, fw, s)));
+      } else if (j == nlaunch - 1) {
+        LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, nb, iters, solver == BSCT_CG, xc, pc, fw, s)));
+      } else {
+        const int it = (j - 1) / 3, ph = (j - 1) % 3;
+        if (ph == 0) {
+          if (solver == BSCT_CG)
+            LAUNCH(p, BSCT_K_PASS_A, 1, (fused_pass_a<T>(p->N, p->L, nb, it, xc, rc, pc, T1c, tw, fw, s)));
+          else
+            LAUNCH(p, BSCT_K_PASS_A, 1, (pass_a<T>(p->N, p->L, nb, rc, T1c, tw, s)));
+        } else if (ph == 1) {
+          LAUNCH(p, BSCT_K_PASS_B, 1,
+                 (pass_b<T>(p->N, p->L, nb, T1c, (const T *)p->S, tw, solver == BSCT_LANDWEBER ? nullptr : fw.gpart, s)));
+        } else {
+          LAUNCH(p, BSCT_K_PASS_C, 1, (fused_pass_c<T>(p->N, p->L, nb, it, solver, gparts, T1c, xc, rc, tw, fw, s)));
+        }
       }
-      LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, nb, iters, solver == BSCT_CG, xc, pp, fw, s)));
+      return BSCT_OK;
+    };
+    const int ns = chunk_streams(p, cb, B);
+    if (ns > 1) {
+      // L2-resident chunks on ns streams: chunk k runs all its iterations on stream k % ns, with
+      // its own workspace slices, so that ns chunks are in flight and fill each other's tails
+      while ((int)p->gstreams.size() < ns) {
+        cudaStream_t gs = nullptr;
+        CU(cudaStreamCreateWithFlags(&gs, cudaStreamNonBlocking));
+        p->gstreams.push_back(gs);
+      }
+      while ((int)p->gevents.size() < 1 + ns) {
+        cudaEvent_t e = nullptr;
+        CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        p->gevents.push_back(e);
+      }
+      CU(cudaEventRecord(p->gevents[0], s));
+      for (int i = 0; i < ns; ++i) CU(cudaStreamWaitEvent(p->gstreams[i], p->gevents[0], 0));
+      const int nch = (B + cb - 1) / cb;
+      for (int k0 = 0; k0 < nch; k0 += ns)
+        for (int j = 0; j < nlaunch; ++j)
+          for (int k = k0; k < std::min(nch, k0 + ns); ++k) {
+            bsct_status st = launch(k * cb, std::min(cb, B - k * cb), true, j, p->gstreams[k % ns]);
+            if (st != BSCT_OK) return st;
+          }
+      for (int i = 0; i < ns; ++i) {
+        CU(cudaEventRecord(p->gevents[1 + i], p->gstreams[i]));
+        CU(cudaStreamWaitEvent(s, p->gevents[1 + i], 0));
+      }
+      return BSCT_OK;
     }
+    for (int c0 = 0; c0 < B; c0 += cb)
+      for (int j = 0; j < nlaunch; ++j) {
+        bsct_status st = launch(c0, std::min(cb, B - c0), false, j, s);
+        if (st != BSCT_OK) return st;
+      }
     return BSCT_OK;
   }
   SolverWork w = solver_work(p, resid, flags);
@@ -884,6 +961,8 @@ bsct_status bsct_plan_destroy(bsct_plan p) {
     if (b) cudaFree(b);
   for (cudaEvent_t e : p->prof_pool) cudaEventDestroy(e);
   for (cudaEvent_t e : p->pipe_ev) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->gevents) cudaEventDestroy(e);
+  for (cudaStream_t g : p->gstreams) cudaStreamDestroy(g);
   if (p->aux) cudaStreamDestroy(p->aux);
   if (p->aux2) cudaStreamDestroy(p->aux2);
   if (p->hi) cudaStreamDestroy(p->hi);

@@ -39,6 +39,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "tma.cuh"
 
 namespace bsct {
 
@@ -50,40 +51,6 @@ constexpr int TC_THREADS = 352;  // 8 W-producer warps, G TMA warp, MMA warp, ta
 constexpr int TC_ROWB = 128;                        // bytes per operand row (32 x FP32)
 constexpr int TC_OPB = TC_M * TC_ROWB;              // one operand tile: 16 KB
 constexpr int HCv = 25;                             // correction filter half-width (R8)
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
-}
-__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
-}
-#ifdef BSCT_TC_DEBUG
-#define TC_DBG(...) printf(__VA_ARGS__)
-#else
-#define TC_DBG(...)
-#endif
-__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity, int who = 0, int a = 0) {
-  uint32_t done = 0;
-  long long it = 0;
-  while (true) {
-    asm volatile(
-        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
-        : "=r"(done)
-        : "r"(bar), "r"(parity)
-        : "memory");
-    if (done) return;
-    if (++it > (1ll << 26)) {  // a lost arrival: fail loudly instead of hanging the GPU
-      TC_DBG("bp_tc timeout: block (%d,%d,%d) thread %d who %d angle %d bar %u parity %u\n", blockIdx.x, blockIdx.y,
-             blockIdx.z, threadIdx.x, who, a, bar, parity);
-      __trap();
-    }
-  }
-}
 
 __device__ __forceinline__ float tf32_rna(float x) {
   uint32_t r;
@@ -118,14 +85,6 @@ __device__ __forceinline__ void umma_tf32(uint32_t dtmem, uint64_t adesc, uint64
 __device__ __forceinline__ void umma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
                : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap *map, int x, int y, int z, uint32_t bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(dst),
-      "l"(map), "r"(x), "r"(y), "r"(z), "r"(bar)
-      : "memory");
 }
 
 }  // namespace
@@ -441,13 +400,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1) bp_tc_kernel(int N, int n_angle
 }
 
 // ------------------------------------------------------------------------------------ host side
-namespace {
-
-using EncodeTiled = CUresult (*)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
-                                 const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
-                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
-
-EncodeTiled encoder() {
+EncodeTiled tma_encoder() {
   static EncodeTiled fn = nullptr;
   static std::once_flag once;
   std::call_once(once, [] {
@@ -460,9 +413,11 @@ EncodeTiled encoder() {
   return fn;
 }
 
+namespace {
+
 // 3-D map over rows [B][n_angles][ldt] FP32 (Mt valid columns): box {32, 1, 128}, SWIZZLE_128B
 bool make_map(CUtensorMap *map, const float *base, int Mt, int ldt, int n_angles, int B) {
-  EncodeTiled enc = encoder();
+  EncodeTiled enc = tma_encoder();
   if (!enc) return false;
   const cuuint64_t dims[3] = {(cuuint64_t)Mt, (cuuint64_t)n_angles, (cuuint64_t)B};
   const cuuint64_t strides[2] = {(cuuint64_t)ldt * 4, (cuuint64_t)ldt * 4 * n_angles};

@@ -1340,6 +1340,8 @@ static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *
       const float2 *twl = tw1024_table();
       if (!twl) return cudaErrorMemoryAllocation;
       constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * (WROWS / 2 + 1);
+      if (pass_c_tma_enabled(N, w.nparts))  // opt-in TMA-pipelined pass C (passes_tma.cu)
+        return pass_c_1024_tma(N, k, MODE, gparts, T1, x, r, twl, w, s);
       cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<MODE, WROWS>, sm);
       if (e != cudaSuccess) return e;
       cg_pass_c_1024_kernel<MODE, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, gparts, T1, x, r, twl, w,
@@ -1528,6 +1530,7 @@ cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaSt
   FusedWork w{};
   w.nparts = fused_parts(N, L, true);
   w.B = B;
+  if (pass_c_tma_enabled(N, w.nparts)) return pass_c_1024_tma(N, 0, 3, 0, T1, nullptr, y, twl, w, s);
   cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<3, WROWS>, sm);
   if (e != cudaSuccess) return e;
   cg_pass_c_1024_kernel<3, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w,

@@ -11,6 +11,8 @@
 // reads are dead code (the zero-padded inputs and cropped outputs of the Toeplitz embedding).
 #pragma once
 
+#include <utility>
+
 #include "common.cuh"
 
 namespace bsct {
@@ -55,12 +57,13 @@ __host__ __device__ constexpr int bitrev5(int x) {
   return ((x & 1) << 4) | ((x & 2) << 2) | (x & 4) | ((x & 8) >> 2) | ((x & 16) >> 4);
 }
 
-// In-register DFT_32: a[k] <- sum_n a[n] exp(-+2 pi i n k / 32), natural order in and out.
+// In-register DFT_32, radix-2 decimation in frequency (the round-1 form, BSCT_DFT32_DIF=1):
+// a[k] <- sum_n a[n] exp(-+2 pi i n k / 32), natural order in and out.
 // HALF_IN: a[16..31] are zero on entry (the zero-padded half of the Toeplitz embedding);
 // the first radix-2 stage then reduces to a twiddle (x + 0 cannot be folded by the
 // compiler without fast-math, so the pruning is explicit).
 template <bool INV, bool HALF_IN = false>
-__device__ __forceinline__ void dft32(float2 *a) {
+__device__ __forceinline__ void dft32_dif(float2 *a) {
   if constexpr (HALF_IN) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) a[j + 16] = twiddle32<INV>(a[j], j);
@@ -82,6 +85,94 @@ __device__ __forceinline__ void dft32(float2 *a) {
   for (int i = 0; i < 32; ++i) o[bitrev5(i)] = a[i];
 #pragma unroll
   for (int i = 0; i < 32; ++i) a[i] = o[i];
+}
+
+// Radix-2 butterfly (e + W o, e - W o), W = exp(-+2 pi i M / 32), with the twiddle folded into
+// the butterfly (Linzer & Feig's FMA form): for W = c (1 + i t), |t| <= 1,
+//   u = (1 + i t) o          one FFMA2 (swapped operand, constants (-t, t))
+//   e +- W o = e +- c u      two FFMA2
+// and for |s| > |c| the same with W = s i (1 - i t), t = c / s.  A twiddled butterfly is 3 FP32x2
+// instructions instead of 4 (complex multiply 2 + add/sub 2); trivial twiddles (M = 0, 8) are 2.
+template <bool INV, int M>
+__device__ __forceinline__ void bfly32(float2 &e, float2 &o) {
+  if constexpr (M == 0) {
+    const float2 a = cadd(e, o), b = csub(e, o);
+    e = a;
+    o = b;
+  } else if constexpr (M == 8) {  // W = -i (forward) / +i (inverse)
+    const float2 wo = INV ? float2{-o.y, o.x} : float2{o.y, -o.x};
+    const float2 a = cadd(e, wo), b = csub(e, wo);
+    e = a;
+    o = b;
+  } else {
+    constexpr double cd = cos32(M), sd = INV ? sin32(M) : -sin32(M);
+    constexpr bool cmaj = (cd < 0 ? -cd : cd) >= (sd < 0 ? -sd : sd);
+#ifdef BSCT_F32X2
+    if constexpr (cmaj) {
+      constexpr float t = (float)(sd / cd), c = (float)cd;
+      const float2 u = x2fma(float2{o.y, o.x}, float2{-t, t}, o), e0 = e;
+      e = x2fma(u, float2{c, c}, e0);
+      o = x2fma(u, float2{-c, -c}, e0);
+    } else {
+      constexpr float t = (float)(cd / sd), sv = (float)sd;
+      const float2 u = x2fma(float2{o.y, o.x}, float2{t, -t}, o), e0 = e;
+      const float2 us{u.y, u.x};
+      e = x2fma(us, float2{-sv, sv}, e0);
+      o = x2fma(us, float2{sv, -sv}, e0);
+    }
+#else
+    const float2 wo = crot(o, (float)cd, (float)sd);
+    const float2 a = cadd(e, wo), b = csub(e, wo);
+    e = a;
+    o = b;
+#endif
+  }
+}
+
+// one radix-2 DIT stage of butterfly span LEN: butterfly F (0..15) of the stage pairs
+// x[blk + j], x[blk + j + LEN / 2] with twiddle index j (32 / LEN)
+template <bool INV, int LEN, int F>
+__device__ __forceinline__ void dit_bfly(float2 *x) {
+  constexpr int H = LEN / 2, blk = (F / H) * LEN, j = F % H;
+  bfly32<INV, j * (32 / LEN)>(x[blk + j], x[blk + j + H]);
+}
+template <bool INV, int LEN, int... F>
+__device__ __forceinline__ void dit_stage(float2 *x, std::integer_sequence<int, F...>) {
+  (dit_bfly<INV, LEN, F>(x), ...);
+}
+
+// In-register DFT_32, radix-2 decimation in time with the twiddles folded into the butterflies
+// (bfly32): a[k] <- sum_n a[n] exp(-+2 pi i n k / 32), natural order in and out (the bit reversal
+// of the input is register renaming).  194 FP32x2 instructions instead of the DIF form's 228;
+// HALF_IN (a[16..31] = 0 on entry): the first stage is a copy (162); outputs a caller never reads
+// are dead code (the last stage's e - W o of the output-pruned inverse transforms).
+template <bool INV, bool HALF_IN = false>
+__device__ __forceinline__ void dft32_dit(float2 *a) {
+  float2 x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) x[i] = a[bitrev5(i)];
+  using Seq = std::make_integer_sequence<int, 16>;
+  if constexpr (HALF_IN) {  // x[2i + 1] = a[bitrev5(2i) + 16] = 0: the first stage copies
+#pragma unroll
+    for (int i = 0; i < 16; ++i) x[2 * i + 1] = x[2 * i];
+  } else {
+    dit_stage<INV, 2>(x, Seq{});
+  }
+  dit_stage<INV, 4>(x, Seq{});
+  dit_stage<INV, 8>(x, Seq{});
+  dit_stage<INV, 16>(x, Seq{});
+  dit_stage<INV, 32>(x, Seq{});
+#pragma unroll
+  for (int i = 0; i < 32; ++i) a[i] = x[i];
+}
+
+template <bool INV, bool HALF_IN = false>
+__device__ __forceinline__ void dft32(float2 *a) {
+#ifdef BSCT_DFT32_DIF
+  dft32_dif<INV, HALF_IN>(a);
+#else
+  dft32_dit<INV, HALF_IN>(a);
+#endif
 }
 
 // cos(2 pi m / 64), compile-time (the W_64 factors of the L = 2048 parity split)
@@ -158,6 +249,27 @@ __device__ __forceinline__ void twiddle1024(float2 *v, const float2 *__restrict_
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
     const float2 b = __ldg(tw + (4 * i) * 32 + lane);
+    if (INV) {
+      if (i) v[4 * i] = cmulc(v[4 * i], b);
+      v[4 * i + 1] = i ? cmulc(cmulc(v[4 * i + 1], b), r1) : cmulc(v[1], r1);
+      v[4 * i + 2] = i ? cmulc(cmulc(v[4 * i + 2], b), r2) : cmulc(v[2], r2);
+      v[4 * i + 3] = i ? cmulc(cmulc(v[4 * i + 3], b), r3) : cmulc(v[3], r3);
+    } else {
+      if (i) v[4 * i] = cmul(v[4 * i], b);
+      v[4 * i + 1] = i ? cmul(cmul(v[4 * i + 1], b), r1) : cmul(v[1], r1);
+      v[4 * i + 2] = i ? cmul(cmul(v[4 * i + 2], b), r2) : cmul(v[2], r2);
+      v[4 * i + 3] = i ? cmul(cmul(v[4 * i + 3], b), r3) : cmul(v[3], r3);
+    }
+  }
+}
+
+// twiddle1024 reading the table through generic loads (e.g. a shared-memory copy)
+template <bool INV>
+__device__ __forceinline__ void twiddle1024_any(float2 *v, const float2 *tw, int lane) {
+  const float2 r1 = tw[1 * 32 + lane], r2 = tw[2 * 32 + lane], r3 = tw[3 * 32 + lane];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float2 b = tw[(4 * i) * 32 + lane];
     if (INV) {
       if (i) v[4 * i] = cmulc(v[4 * i], b);
       v[4 * i + 1] = i ? cmulc(cmulc(v[4 * i + 1], b), r1) : cmulc(v[1], r1);
