@@ -527,8 +527,7 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
   // the key includes every switch that selects the launched code path
   const intptr_t path = (onchip_enabled() ? 1 : 0) | (pass_b_warp_enabled() ? 2 : 0) | (pass_c_warp_enabled() ? 4 : 0) |
                         (bulk_stage_enabled() ? 8 : 0) | (p->solver_v1 ? 16 : 0) |
-                        ((intptr_t)cb << 8) | ((intptr_t)ns << 40) |
-                        ((getenv("BSCT_PASSC_TMA") && getenv("BSCT_PASSC_TMA")[0] == '1') ? 32 : 0);
+                        ((intptr_t)cb << 8) | ((intptr_t)ns << 40);
   const void *key[8] = {b, x, (const void *)(intptr_t)B, (const void *)(intptr_t)iters,
                         (const void *)(intptr_t)solver, resid, flags, (const void *)path};
   for (auto &gk : p->graphs)

@@ -1197,10 +1197,12 @@ static int fused_parts_L(int N) {
   return (N + 2 * G - 1) / (2 * G);
 }
 
-// rows per CTA of the FP32 L = 1024 warp-FFT passes A and C (2 rows per warp); 8 rows (4
-// CTAs/SM instead of 2) measured 3% slower on config 5
+// rows per CTA of the FP32 L = 1024 warp-FFT passes A and C (2 rows per warp).  Round 1 (whole-
+// batch launches, HBM-resident): 16 rows (2 CTAs/SM) 3% faster than 8; round 2 (L2-resident solver
+// chunks, api.cu): 8 rows (4 CTAs/SM, more independent tiles per SM) 3% faster (config 5 CG 325 ->
+// 315 ms per 2048 x 50, profiles/r02/wrows_ab.txt)
 #ifndef BSCT_WROWS
-#define BSCT_WROWS 16
+#define BSCT_WROWS 8
 #endif
 constexpr int WROWS = BSCT_WROWS;
 
@@ -1340,8 +1342,6 @@ static cudaError_t cg_pass_c_LM(int N, int B, int k, int gparts, const cplx<T> *
       const float2 *twl = tw1024_table();
       if (!twl) return cudaErrorMemoryAllocation;
       constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * (WROWS / 2 + 1);
-      if (pass_c_tma_enabled(N, w.nparts))  // opt-in TMA-pipelined pass C (passes_tma.cu)
-        return pass_c_1024_tma(N, k, MODE, gparts, T1, x, r, twl, w, s);
       cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<MODE, WROWS>, sm);
       if (e != cudaSuccess) return e;
       cg_pass_c_1024_kernel<MODE, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, gparts, T1, x, r, twl, w,
@@ -1530,7 +1530,6 @@ cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaSt
   FusedWork w{};
   w.nparts = fused_parts(N, L, true);
   w.B = B;
-  if (pass_c_tma_enabled(N, w.nparts)) return pass_c_1024_tma(N, 0, 3, 0, T1, nullptr, y, twl, w, s);
   cudaError_t e = cg_set_smem(cg_pass_c_1024_kernel<3, WROWS>, sm);
   if (e != cudaSuccess) return e;
   cg_pass_c_1024_kernel<3, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, 0, 0, T1, nullptr, y, twl, w,

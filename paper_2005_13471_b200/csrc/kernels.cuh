@@ -158,11 +158,6 @@ struct SolverWork {
 int vec_blocks(int N);
 
 // fused solver iteration (cg.cu): pass A(CG) / pass C with the vector updates folded in
-struct FusedWork;
-// persistent TMA-pipelined pass C at L = 1024 (passes_tma.cu); BSCT_PASSC_TMA=0 disables it
-bool pass_c_tma_enabled(int N, int nparts);
-cudaError_t pass_c_1024_tma(int N, int k, int mode, int gparts, const float2 *T1, float *x, float *r,
-                            const float2 *twl, const FusedWork &w, cudaStream_t s);
 struct FusedWork {
   double *rho;     // [B][rho_stride]
   int rho_stride;

@@ -1,6 +1,5 @@
 // tma.cuh -- mbarrier and TMA (cp.async.bulk / cp.async.bulk.tensor) helpers shared by the kernels
-// that stage operands with the sm_100 copy engine: K4 v4 (bp_tc.cu) and the TMA-pipelined CG
-// pass C (passes_tma.cu).
+// that stage operands with the sm_100 copy engine (K4 v4, bp_tc.cu).
 #pragma once
 
 #include <cuda.h>

@@ -1,6 +1,6 @@
 """L2-resident solver chunks on several streams (api.cu, BSCT_CG_CHUNK / BSCT_CHUNK_STREAMS: chunk k
 of the batch runs all its iterations on stream k % ns with its own workspace slices, captured into
-a CUDA graph), and the opt-in TMA-pipelined pass C.  Slices are independent (one CG per
+a CUDA graph).  Slices are independent (one CG per
 slice), so a chunked solve must equal the plain one bit for bit -- x, the residual history and the
 breakdown flags -- for CG, steepest descent and Landweber, with a ragged last chunk."""
 import numpy as np
@@ -69,28 +69,3 @@ def test_default_chunking_bitwise(cuda_lib, monkeypatch):
     for o in xs[1:]:
         for a, c in zip(xs[0], o):
             assert torch.equal(a, c)
-
-
-@pytest.mark.parametrize("solver", ["cg", "sd", "landweber"])
-def test_pass_c_tma_matches(cuda_lib, monkeypatch, solver):
-    """The opt-in TMA-pipelined pass C (passes_tma.cu, BSCT_PASSC_TMA=1) against
-    cg_pass_c_1024_kernel: same per-tile arithmetic, scalar reductions in another fixed order."""
-    import torch
-    cfg = CONFIGS[5]
-    g = cfg.geometry()
-    N, B, K = cfg.N, 5, 6
-    plan, _ = gpu_plan(cuda_lib, g, "f32", max_batch=B)
-    torch.manual_seed(5)
-    b = torch.rand((B, N, N), device="cuda")
-    xs = []
-    for tma in ("0", "1"):
-        monkeypatch.setenv("BSCT_PASSC_TMA", tma)
-        monkeypatch.setenv("BSCT_GRAPH", "0")
-        x = torch.empty((B, N, N), device="cuda")
-        cuda_lib.cg_solve(plan, b, x, K, solver)
-        y = torch.empty_like(b)
-        cuda_lib.normal_apply(plan, b, y)
-        torch.cuda.synchronize()
-        xs.append((x.double().cpu(), y.double().cpu()))
-    for a, c in zip(*xs):
-        assert float((a - c).norm() / c.norm()) < 1e-6
