@@ -15,6 +15,7 @@
 #include "fft.cuh"
 #include "fft32.cuh"
 
+#include <algorithm>
 #include <cstdlib>
 #include <type_traits>
 #include "kernels.cuh"
@@ -221,6 +222,12 @@ __global__ void __launch_bounds__(FftLaunch<L>::THREADS) cg_pass_a_kernel(int N,
   }
 }
 
+// 16-byte cp.async global -> shared, zero-filling the bytes past src_bytes (0 or 16)
+__device__ __forceinline__ void cp_async16z(void *dst, const void *src, int src_bytes) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(d), "l"(src), "r"(src_bytes));
+}
+
 // ---------------------------------------------------------------- pass A (CG), L = 1024 (FP32 warp FFTs)
 // Same contract as cg_pass_a_kernel (16 rows per CTA).  Streaming phase: x += alpha p,
 // p = r + beta p with 16-byte accesses, the new p rows kept in shared memory; each warp
@@ -263,49 +270,90 @@ __global__ void __launch_bounds__(ROWS * 16, 32 / ROWS) cg_pass_a_1024_kernel(in
   const int row0 = blockIdx.x * ROWS;
   const int rows = min(ROWS, N - row0);
   const size_t so = (size_t)b * N * N + (size_t)row0 * N;
-  // streaming phase (VW-wide): x += a p_old, p = r + b p_old; p rows -> ps, zero-padded to PW
-  // batches of UB items per thread: all 3 UB loads are issued before the first use
-  constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
-  static_assert(ITEMS % (UB * NT) == 0, "every thread runs the same number of batches (the first one reduces)");
-  for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
-    float pv[UB][VW], rv[UB][VW], xv[UB][VW];
-    bool ok[UB];
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int i = i0 + u * NT;
-      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
-      ok[u] = i < ITEMS && rr < rows && j < N;
-      if (ok[u]) {
-        const size_t e = so + (size_t)rr * N + j;
-        vload<float, VW>(pv[u], p + e);
-        if (!PLAIN) {
-          vload<float, VW>(rv[u], r + e);
-          vload<float, VW>(xv[u], x + e);
+  if constexpr (VW == 4) {
+    // streaming phase, 16-byte rows: the CTA's p (and r, x) rows are copied into shared memory by
+    // cp.async (columns >= N and rows >= N zero-filled), so that all of its loads are in flight at
+    // once while the scalars are reduced; then x += a p_old, p = r + b p_old in place, written back
+    float *sp = ps, *sr = ps + ROWS * PW, *sx = ps + 2 * ROWS * PW;
+    constexpr int CH = ROWS * (PW / 4);  // 16-byte chunks per array
+    for (int i = threadIdx.x; i < CH; i += NT) {
+      const int rr = i / (PW / 4), j = (i - rr * (PW / 4)) * 4;
+      const bool ok = rr < rows && j < N;
+      const size_t e = ok ? so + (size_t)rr * N + j : so;
+      const int o = rr * PW + j, nb = ok ? 16 : 0;
+      cp_async16z(sp + o, p + e, nb);
+      if (!PLAIN) {
+        cp_async16z(sr + o, r + e, nb);
+        cp_async16z(sx + o, x + e, nb);
+      }
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+    scalars();
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
+    if (!PLAIN) {
+      for (int i = threadIdx.x; i < CH; i += NT) {
+        const int rr = i / (PW / 4), j = (i - rr * (PW / 4)) * 4;
+        if (rr < rows && j < N) {
+          const int o = rr * PW + j;
+          const float4 pv = *reinterpret_cast<const float4 *>(sp + o), rv = *reinterpret_cast<const float4 *>(sr + o),
+                       xv = *reinterpret_cast<const float4 *>(sx + o);
+          const float4 xn = make_float4(fmaf(al, pv.x, xv.x), fmaf(al, pv.y, xv.y), fmaf(al, pv.z, xv.z),
+                                        fmaf(al, pv.w, xv.w));
+          const float4 pn = make_float4(fmaf(be, pv.x, rv.x), fmaf(be, pv.y, rv.y), fmaf(be, pv.z, rv.z),
+                                        fmaf(be, pv.w, rv.w));
+          const size_t e = so + (size_t)rr * N + j;
+          *reinterpret_cast<float4 *>(x + e) = xn;
+          *reinterpret_cast<float4 *>(p + e) = pn;
+          *reinterpret_cast<float4 *>(sp + o) = pn;
         }
       }
     }
-    if (i0 == (int)threadIdx.x) scalars();  // first batch: uniform across the CTA
-#pragma unroll
-    for (int u = 0; u < UB; ++u) {
-      const int i = i0 + u * NT;
-      if (i >= ITEMS) break;
-      const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
-      if (ok[u]) {
-        if (!PLAIN) {
+  } else {
+    // streaming phase (VW-wide): x += a p_old, p = r + b p_old; p rows -> ps, zero-padded to PW
+    // batches of UB items per thread: all 3 UB loads are issued before the first use
+    constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
+    static_assert(ITEMS % (UB * NT) == 0, "every thread runs the same number of batches (the first one reduces)");
+    for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
+      float pv[UB][VW], rv[UB][VW], xv[UB][VW];
+      bool ok[UB];
+  #pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int i = i0 + u * NT;
+        const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+        ok[u] = i < ITEMS && rr < rows && j < N;
+        if (ok[u]) {
           const size_t e = so + (size_t)rr * N + j;
-#pragma unroll
-          for (int c = 0; c < VW; ++c) {
-            xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
-            pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+          vload<float, VW>(pv[u], p + e);
+          if (!PLAIN) {
+            vload<float, VW>(rv[u], r + e);
+            vload<float, VW>(xv[u], x + e);
           }
-          vstore<float, VW>(x + e, xv[u]);
-          vstore<float, VW>(p + e, pv[u]);
         }
-      } else {
-#pragma unroll
-        for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
       }
-      vstore<float, VW>(ps + rr * PW + j, pv[u]);
+      if (i0 == (int)threadIdx.x) scalars();  // first batch: uniform across the CTA
+  #pragma unroll
+      for (int u = 0; u < UB; ++u) {
+        const int i = i0 + u * NT;
+        if (i >= ITEMS) break;
+        const int rr = i / (PW / VW), j = (i - rr * (PW / VW)) * VW;
+        if (ok[u]) {
+          if (!PLAIN) {
+            const size_t e = so + (size_t)rr * N + j;
+  #pragma unroll
+            for (int c = 0; c < VW; ++c) {
+              xv[u][c] = fmaf(al, pv[u][c], xv[u][c]);
+              pv[u][c] = fmaf(be, pv[u][c], rv[u][c]);
+            }
+            vstore<float, VW>(x + e, xv[u]);
+            vstore<float, VW>(p + e, pv[u]);
+          }
+        } else {
+  #pragma unroll
+          for (int c = 0; c < VW; ++c) pv[u][c] = 0.f;
+        }
+        vstore<float, VW>(ps + rr * PW + j, pv[u]);
+      }
     }
   }
   __syncthreads();
@@ -1230,7 +1278,8 @@ constexpr size_t cg_smem(size_t elem) { return (size_t)FftLaunch<L>::G * FftCfg<
 
 template <typename K>
 static cudaError_t cg_set_smem(K kernel, size_t bytes) {
-  if (bytes > 48 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  // dynamic + static shared memory above 48 KB needs the opt-in (the kernels' static parts are ~1-2 KB)
+  if (bytes > 40 * 1024) return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
   return cudaSuccess;
 }
 
@@ -1272,10 +1321,11 @@ static cudaError_t cg_pass_a_L(int N, int B, int k, T *x, const T *r, T *p, cplx
       const float2 *twl = tw1024_table();
       if (!twl) return cudaErrorMemoryAllocation;
       constexpr size_t sm = sizeof(float4) * (L / 2 + 1) * (WROWS / 2 + 1);
+      constexpr size_t sm4 = std::max(sm, sizeof(float) * 3 * WROWS * 512);  // + the cp.async row staging
       if (can_vec<T>(N, x, r, p)) {
-        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, false, WROWS>, sm);
+        cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<4, false, WROWS>, sm4);
         if (e != cudaSuccess) return e;
-        cg_pass_a_1024_kernel<4, false, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm, s>>>(N, k, x, r, p, T1, twl, w);
+        cg_pass_a_1024_kernel<4, false, WROWS><<<dim3(w.nparts, B), WROWS * 16, sm4, s>>>(N, k, x, r, p, T1, twl, w);
       } else {
         cudaError_t e = cg_set_smem(cg_pass_a_1024_kernel<1, false, WROWS>, sm);
         if (e != cudaSuccess) return e;
