@@ -521,7 +521,9 @@ bsct_status solve_t(bsct_plan p, const T *b, T *x, int B, int iters, int solver,
   // captured as well, so that the host enqueue does not bound them
   const int cb = solver_chunk(p, B);
   const int ns = chunk_streams(p, cb, B);
-  const bool graph = !(ge && ge[0] == '0') && !p->prof_on &&
+  // the persistent solver is 3 launches per solve: nothing to capture
+  const bool persist = !p->solver_v1 && persist_enabled(p->L, p->dt == BSCT_F32, B, solver == BSCT_CG);
+  const bool graph = !(ge && ge[0] == '0') && !p->prof_on && !persist &&
                      ((size_t)B * p->N * p->N <= ((size_t)1 << 22) || ns > 1);
   if (!graph) return solve_launch_t<T>(p, b, x, B, iters, solver, resid, flags, s);
   // the key includes every switch that selects the launched code path
@@ -592,6 +594,28 @@ bsct_status solve_launch_t(bsct_plan p, const T *b, T *x, int B, int iters, int 
     // final) of the chunk of nb slices from slice c0, on stream s; ws: workspaces at the chunk's
     // own offsets (concurrent groups) or shared (sequential chunks)
     const int nlaunch = 3 * iters + 2;
+    if constexpr (std::is_same<T, float>::value) {
+      if (persist_enabled(p->L, true, B, solver == BSCT_CG)) {
+        // small batches at L = 2048: init, every iteration in one cooperative launch, finish
+        FusedWork fw;
+        fw.rho = p->rho;
+        fw.rho_stride = iters + 1;
+        fw.alpha = p->alpha;
+        fw.gpart = p->gpart;
+        fw.rpart = p->rpart;
+        fw.nparts = nparts;
+        fw.B = B;
+        fw.flags = flags ? flags : p->flags;
+        fw.resid = resid;
+        fw.iters = iters;
+        fw.tau = p->tau;
+        LAUNCH(p, BSCT_K_SOLVER_INIT, 1, (fused_init<T>(p->N, B, b, x, r, pp, fw, s)));
+        LAUNCH(p, BSCT_K_FUSED_CG, 1,
+               (persist_cg_2048(p->N, B, iters, x, r, pp, T1, (const float *)p->S, fw, gparts, s)));
+        LAUNCH(p, BSCT_K_SOLVER_FINISH, 1, (fused_final<T>(p->N, B, iters, 1, x, pp, fw, s)));
+        return BSCT_OK;
+      }
+    }
     auto launch = [&](int c0, int nb, bool ws, int j, cudaStream_t s) -> bsct_status {
       const T *bc = b + c0 * nn;
       T *xc = x + c0 * nn;

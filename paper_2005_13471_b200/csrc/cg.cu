@@ -14,6 +14,9 @@
 // previous partials while writing the next ones.
 #include "fft.cuh"
 #include "fft32.cuh"
+#include "pass_b2048.cuh"
+
+#include <cooperative_groups.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -563,21 +566,21 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_512_kernel(int N, int k, flo
 // lane (32 - m) mod 32, register 31 - k for e = 0 (lane 0: its own register (32 - k) mod 32) and
 // lane 31 - m, register 31 - k for e = 1 -- one shuffle per register.  T1[q][row0 .. row0 + 8)
 // is written through a [q parity][q / 2][5] float4 staging tile (64 contiguous bytes per q).
-template <int VW, bool PLAIN>
-__global__ void __launch_bounds__(256, 2) cg_pass_a_2048_kernel(int N, int k, float *__restrict__ x,
-                                                                const float *__restrict__ r, float *__restrict__ p,
-                                                                float2 *__restrict__ T1,
-                                                                const float2 *__restrict__ tw2, FusedWork w) {
+// Tile bx (rows 8 bx .. 8 bx + 7) of slice b; 256 threads; smem: the dynamic shared memory.
+// The caller synchronises the CTA before reusing smem for another tile.
+template <int VW, bool PLAIN, int UB = 4>
+__device__ __forceinline__ void cg_pass_a_2048_tile(int bx, int b, int N, int k, float *__restrict__ x,
+                                                    const float *__restrict__ r, float *__restrict__ p,
+                                                    float2 *__restrict__ T1, const float2 *__restrict__ tw2,
+                                                    FusedWork w, unsigned char *smem_raw) {
   constexpr int L = 2048, Q = L / 2 + 1, ROWS = 8, NP = ROWS / 2, RS = NP + 1, HALF = L / 4 + 1;
   constexpr int PW = 1024, PWS = 1032, NT = 256;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   float *ps = reinterpret_cast<float *>(smem_raw);    // [ROWS][PWS] new p rows
   float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [2][HALF][RS] output staging (after the FFTs)
   float2 *trb = reinterpret_cast<float2 *>(smem_raw); // [8][32][33] transposes
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, e = warp & 1;
-  const int b = blockIdx.y;
   float be = 0.f, al = 0.f;
   auto scalars = [&]() {
     if (PLAIN) return;
@@ -588,17 +591,17 @@ __global__ void __launch_bounds__(256, 2) cg_pass_a_2048_kernel(int N, int k, fl
       beta = rho_prev > 0 ? rho / rho_prev : 0.0;
       alpha_prev = w.alpha[b];
     }
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (bx == 0 && threadIdx.x == 0) {
       w.rho[(size_t)b * w.rho_stride + k] = rho;
       if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
     }
     be = (float)beta;
     al = (float)alpha_prev;
   };
-  const int row0 = blockIdx.x * ROWS;
+  const int row0 = bx * ROWS;
   const int rows = min(ROWS, N - row0);
   const size_t so = (size_t)b * N * N + (size_t)row0 * N;
-  constexpr int ITEMS = ROWS * (PW / VW), UB = 4;
+  constexpr int ITEMS = ROWS * (PW / VW);  // UB: row batches in flight per thread
   static_assert(ITEMS % (UB * NT) == 0, "every thread runs the same number of batches (the first one reduces)");
   for (int i0 = threadIdx.x; i0 < ITEMS; i0 += UB * NT) {
     float pv[UB][VW], rv[UB][VW], xv[UB][VW];
@@ -686,6 +689,15 @@ twiddle2048_fwd(v, tw2, e, lane);  // W_2048^{(2m + e) t}
       dst[0] = float2{c.x, c.y};
     }
   }
+}
+
+template <int VW, bool PLAIN>
+__global__ void __launch_bounds__(256, 2) cg_pass_a_2048_kernel(int N, int k, float *__restrict__ x,
+                                                                const float *__restrict__ r, float *__restrict__ p,
+                                                                float2 *__restrict__ T1,
+                                                                const float2 *__restrict__ tw2, FusedWork w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg_pass_a_2048_tile<VW, PLAIN>(blockIdx.x, blockIdx.y, N, k, x, r, p, T1, tw2, w, smem_raw);
 }
 
 // ---------------------------------------------------------------- pass C: inverse row DFTs fused with the r update
@@ -1100,18 +1112,19 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_512_kernel(int N, int k, int
 // m, * W_64^{-r e}; the two warps swap halves through their transpose buffers and warp e
 // updates r (and x) of row a (e = 0) or b (e = 1) of the pair (z = y_a + i y_b, outputs r < 32
 // only: N <= 1024), its r row prefetched into registers before the FFT.
+// Tile bx (rows 8 bx .. 8 bx + 7) of slice b; 256 threads; the caller synchronises the CTA
+// before reusing smem for another tile.
 template <int MODE>
-__global__ void __launch_bounds__(256, 2) cg_pass_c_2048_kernel(int N, int k, int gparts, const float2 *__restrict__ T1,
-                                                                float *__restrict__ x, float *__restrict__ r,
-                                                                const float2 *__restrict__ tw2, FusedWork w) {
+__device__ __forceinline__ void cg_pass_c_2048_tile(int bx, int b, int N, int k, int gparts,
+                                                    const float2 *__restrict__ T1, float *__restrict__ x,
+                                                    float *__restrict__ r, const float2 *__restrict__ tw2,
+                                                    FusedWork w, unsigned char *smem_raw) {
   constexpr int L = 2048, Q = L / 2 + 1, ROWS = 8, NP = ROWS / 2, RS = NP + 1, HALF = L / 4 + 1;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   float4 *st = reinterpret_cast<float4 *>(smem_raw);  // [2][HALF][RS], later [8][32][33] float2
   __shared__ double red[32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = warp >> 1, e = warp & 1;
-  const int b = blockIdx.y;
-  const int row0 = blockIdx.x * ROWS;
+  const int row0 = bx * ROWS;
   const int rows = min(ROWS, N - row0);
   const float2 *T1s = T1 + (size_t)b * Q * N + row0;
   auto slot = [&](int q) { return st + ((q & 1) * HALF + (q >> 1)) * RS; };
@@ -1140,7 +1153,7 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_2048_kernel(int N, int k, in
     rho = w.rho[(size_t)b * w.rho_stride + k];
   } else {
     rho = cta_reduce_parts(w.rpart + ((size_t)(k & 1) * w.B + b) * w.nparts, w.nparts, red);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    if (bx == 0 && threadIdx.x == 0) {
       w.rho[(size_t)b * w.rho_stride + k] = rho;
       if (k > 0 && w.resid) w.resid[(size_t)b * w.iters + k - 1] = sqrt(rho);
     }
@@ -1154,9 +1167,9 @@ __global__ void __launch_bounds__(256, 2) cg_pass_c_2048_kernel(int N, int k, in
     const bool bad = rho > 0 && !(gam > 0);
     const bool frozen = bad || (w.flags && w.flags[b]);
     alpha = (rho > 0 && !frozen) ? rho / gam : 0.0;
-    if (blockIdx.x == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
+    if (bx == 0 && threadIdx.x == 0 && bad && w.flags) w.flags[b] = 1;
   }
-  if (MODE != 3 && blockIdx.x == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
+  if (MODE != 3 && bx == 0 && threadIdx.x == 0) w.alpha[b] = alpha;
   const float al = (float)alpha;
   // this warp's row (a for e = 0, b for e = 1) of r into registers: latency overlaps the FFT
   const int row = row0 + 2 * pair + e;
@@ -1217,7 +1230,15 @@ twiddle2048_inv(v, tw2, e, lane);  // conj W_2048^{(2 lane + e) t}
   }
   if (MODE == 3) return;
   const double s = cta_sum((double)ac, red);
-  if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + blockIdx.x] = s;
+  if (threadIdx.x == 0) w.rpart[((size_t)((k + 1) & 1) * w.B + b) * w.nparts + bx] = s;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 2) cg_pass_c_2048_kernel(int N, int k, int gparts, const float2 *__restrict__ T1,
+                                                                float *__restrict__ x, float *__restrict__ r,
+                                                                const float2 *__restrict__ tw2, FusedWork w) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cg_pass_c_2048_tile<MODE>(blockIdx.x, blockIdx.y, N, k, gparts, T1, x, r, tw2, w, smem_raw);
 }
 
 // ---------------------------------------------------------------- final: rho_K, resid, CG x update
@@ -1236,6 +1257,53 @@ __global__ void __launch_bounds__(256) cg_final_kernel(long n, int K, int cg, T 
   const size_t off = (size_t)b * n;
   for (long i = (long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x)
     x[off + i] = fma(al, p[off + i], x[off + i]);
+}
+
+// ---------------------------------------------------------------- persistent CG, FP32 L = 2048
+// Small batches of large slices (config 4: one 1024^2 slice, 128 pass-A/C tiles and 257
+// four-column pass-B tiles per iteration) leave most of the GPU idle between three dependent
+// launches.  Opt-in (BSCT_PERSIST=1, measured slower: persist_enabled below): one cooperative
+// launch runs all K iterations instead: each CTA loops over the
+// tiles of a pass (the same tile functions as the per-pass kernels, so every value, partial
+// and scalar is formed exactly as there), and a grid barrier separates the passes.  The whole
+// working set (T1 8.4 MB + x, r, p 12.6 MB per slice) stays in L2 across iterations.
+constexpr int PERSIST_BCOLS = 4;  // pass-B columns per tile (256 threads)
+#ifndef BSCT_PERSIST_UB
+#define BSCT_PERSIST_UB 2
+#endif
+constexpr int PERSIST_UB = BSCT_PERSIST_UB;  // pass-A row batches in flight (4 spills in the persistent kernel)
+
+#ifndef BSCT_PERSIST_MINB
+#define BSCT_PERSIST_MINB 2
+#endif
+template <int VW, bool FULL>
+__global__ void __launch_bounds__(256, BSCT_PERSIST_MINB) cg_persist_2048_kernel(int N, int B, int iters, float *__restrict__ x,
+                                                                 float *__restrict__ r, float *__restrict__ p,
+                                                                 float2 *__restrict__ T1, const float *__restrict__ S,
+                                                                 const float2 *__restrict__ tw2, FusedWork w,
+                                                                 int gparts, int skip) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cooperative_groups::grid_group grid = cooperative_groups::this_grid();
+  constexpr int TB = (2048 / 2 + 1 + PERSIST_BCOLS - 1) / PERSIST_BCOLS;  // pass-B tiles per slice
+  const int na = w.nparts * B, nb = TB * B;
+  for (int k = 0; k < iters; ++k) {
+    for (int t = blockIdx.x; t < ((skip & 1) ? 0 : na); t += gridDim.x) {
+      cg_pass_a_2048_tile<VW, false, PERSIST_UB>(t % w.nparts, t / w.nparts, N, k, x, r, p, T1, tw2, w, smem_raw);
+      __syncthreads();
+    }
+    grid.sync();
+    for (int t = blockIdx.x; t < ((skip & 2) ? 0 : nb); t += gridDim.x) {
+      pass_b_2048_tile<FULL, PERSIST_BCOLS>(t % TB, t / TB, gparts, N, T1, S, tw2, w.gpart,
+                                            reinterpret_cast<float2 *>(smem_raw));
+      __syncthreads();
+    }
+    grid.sync();
+    for (int t = blockIdx.x; t < ((skip & 4) ? 0 : na); t += gridDim.x) {
+      cg_pass_c_2048_tile<0>(t % w.nparts, t / w.nparts, N, k, gparts, T1, x, r, tw2, w, smem_raw);
+      __syncthreads();
+    }
+    grid.sync();
+  }
 }
 
 // ---------------------------------------------------------------- launchers
@@ -1598,5 +1666,47 @@ cudaError_t warp_apply_c(int N, int L, int B, const float2 *T1, float *y, cudaSt
   template cudaError_t fused_export<T>(int, int, int, const T *, const T *, T *, T *, FusedWork, cudaStream_t);
 CG_INST(float)
 CG_INST(double)
+
+// BSCT_PERSIST=1: run the persistent solver for FP32 L = 2048 CG (opt-in).  Measured slower than
+// the per-pass launches replayed from a CUDA graph (config 4, B = 1: 51 vs 24 us per iteration;
+// B = 16: 24 vs 17.5 us per slice-iteration; profiles/r02/persist_probe.txt): the three grid
+// barriers cost ~4 us per iteration, and the tiles run slower in the fused kernel (one register
+// budget for all three passes: spills at 2 CTAs/SM, half the pass-B warps at 1 CTA/SM) than as
+// separate kernels, whose own launch gaps the graph already hides.  Single-slice iterations are
+// bound by the per-warp latency of the tiles, not by launches.
+bool persist_enabled(int L, bool fp32, int B, int solver_cg) {
+  (void)B;
+  if (!(fp32 && L == 2048 && solver_cg && pass_c_warp_enabled() && pass_b_warp_enabled())) return false;
+  const char *e = getenv("BSCT_PERSIST");
+  return e && e[0] == '1';
+}
+
+cudaError_t persist_cg_2048(int N, int B, int iters, float *x, float *r, float *p, float2 *T1, const float *S,
+                            FusedWork w, int gparts, cudaStream_t s) {
+  if (N > 1024 || iters <= 0) return iters <= 0 ? cudaSuccess : cudaErrorInvalidValue;
+  const float2 *tw2 = tw2048_table();
+  if (!tw2) return cudaErrorMemoryAllocation;
+  constexpr size_t sm_ac = sizeof(float4) * 2 * (2048 / 4 + 1) * 5;
+  constexpr size_t sm = std::max(sm_ac, pass_b_2048_smem<PERSIST_BCOLS>());
+  const bool vec = can_vec<float>(N, x, r, p), full = N == 1024;
+  void (*kern)(int, int, int, float *, float *, float *, float2 *, const float *, const float2 *, FusedWork, int,
+               int) =
+      vec ? (full ? cg_persist_2048_kernel<4, true> : cg_persist_2048_kernel<4, false>)
+          : (full ? cg_persist_2048_kernel<1, true> : cg_persist_2048_kernel<1, false>);
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per = 0;
+  if ((e = cudaGetDevice(&dev)) != cudaSuccess) return e;
+  if ((e = cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev)) != cudaSuccess) return e;
+  if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kern, 256, sm)) != cudaSuccess) return e;
+  if (per < 1) return cudaErrorLaunchOutOfResources;
+  constexpr int TB = (2048 / 2 + 1 + PERSIST_BCOLS - 1) / PERSIST_BCOLS;
+  const int grid = std::min(per * nsm, std::max(w.nparts * B, TB * B));
+  // BSCT_PERSIST_SKIP (timing probes only: the result is wrong): bit 0/1/2 skips the pass A/B/C tiles
+  const char *sk = getenv("BSCT_PERSIST_SKIP");
+  int skip = sk ? atoi(sk) : 0;
+  void *args[] = {&N, &B, &iters, &x, &r, &p, &T1, (void *)&S, (void *)&tw2, &w, &gparts, &skip};
+  return cudaLaunchCooperativeKernel((const void *)kern, dim3(grid), dim3(256), args, sm, s);
+}
 
 }  // namespace bsct

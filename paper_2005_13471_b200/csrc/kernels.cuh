@@ -189,6 +189,10 @@ cudaError_t fused_pass_a(int N, int L, int B, int k, T *x, const T *r, T *p, cpl
 template <typename T>
 cudaError_t fused_pass_c(int N, int L, int B, int k, int mode, int gparts, const cplx<T> *T1, T *x, T *r,
                          const cplx<T> *tw, FusedWork w, cudaStream_t s);
+// persistent single-launch CG iterations (FP32, L = 2048, small B; cg.cu)
+bool persist_enabled(int L, bool fp32, int B, int solver_cg);
+cudaError_t persist_cg_2048(int N, int B, int iters, float *x, float *r, float *p, float2 *T1, const float *S,
+                            FusedWork w, int gparts, cudaStream_t s);
 template <typename T>
 cudaError_t fused_final(int N, int B, int K, int cg, T *x, const T *p, FusedWork w, cudaStream_t s);
 // resume from a saved state (x_j, r_j, p_j): r = r_in, p = q = p_in, partials of <r_j, r_j>

@@ -11,6 +11,7 @@
 // (Parseval; pad(x) is zero outside the crop) is reduced in pass B for the solvers.
 #include "fft.cuh"
 #include "fft32.cuh"
+#include "pass_b2048.cuh"
 
 #include <cmath>
 #include <cstdlib>
@@ -207,16 +208,7 @@ __global__ void __launch_bounds__(PB_WARPS * 32, 4) pass_b_1024_kernel(int N, fl
 }
 
 // ---------------------------------------------------------------- pass B, L = 2048 (FP32)
-// Two warps per column, 64 x 32 four-step FFT split by the parity e of the first-stage index:
-// lane t holds x[t + 32 r] (r < 32: rows >= N <= 1024 are zero), and warp e = 0, 1 computes
-//   v[m] = DFT_32 over r of x_r W_64^{r e}          (= Y[2m + e], the half-input DFT_64)
-//   * W_2048^{t (2m + e)}, transpose, DFT_32 over t  -> X[2 lane + e + 64 k]
-//   * S, Parseval, and the same steps backwards, ending in
-//   z_e[t + 32 r] = W_64^{-r e} IDFT_32 over m of U[2m + e][t]
-// so only 32 complex values per lane are live; warp 1 hands z_1 to warp 0 through shared
-// memory, which stores z_0 + z_1.  Twiddles come from tw2048_table() through L1:
-// [e][m][t] = W_2048^{(2m + e) t} (forward, coalesced over t) and [2 + e][t][m] (inverse,
-// coalesced over m).
+// Two warps per column (pass_b2048.cuh), PB2_COLS columns per CTA.
 constexpr int PB2_COLS = 2;  // columns per CTA (2 warps each)
 
 template <bool FULL>
@@ -224,65 +216,8 @@ __global__ void __launch_bounds__(PB2_COLS * 64, 4) pass_b_2048_kernel(int N, fl
                                                                      const float *__restrict__ S,
                                                                      const float2 *__restrict__ tw2,
                                                                      double *__restrict__ gpart) {
-  constexpr int L = 2048, Q = L / 2 + 1, NWP = 2 * PB2_COLS;
-  extern __shared__ __align__(16) float2 pb2_smem[];  // [NWP][32 * 33] transposes, [PB2_COLS][32 * 32] z_1
-  __shared__ double red[NWP];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = warp >> 1, e = warp & 1;
-  const int b = blockIdx.y;
-  const int q0 = blockIdx.x * PB2_COLS + c;
-  const bool live = q0 < Q;  // warps past the last column recompute column Q - 1, store nothing
-  const int q = live ? q0 : Q - 1;
-  float2 *col = T1 + ((size_t)b * Q + q) * N;
-  float2 *tr = pb2_smem + warp * (32 * 33), *zx = pb2_smem + NWP * (32 * 33) + c * (32 * 32);
-  const float *Sq = S + (size_t)q * L + 2 * lane + e;
-  float2 v[32];
-#pragma unroll
-  for (int r = 0; r < 32; ++r) {
-    const int n = lane + 32 * r;
-    const float2 xv = (FULL || n < N) ? col[n] : float2{0.f, 0.f};
-    v[r] = e ? twiddle64<false>(xv, r) : xv;  // x_r W_64^{r e}
-  }
-  dft32<false>(v);  // v[m] = Y[2m + e]
-twiddle2048_fwd(v, tw2, e, lane);  // W_2048^{(2m + e) t}
-  warp_transpose32(v, tr, lane);  // lane m: v[t]
-  dft32<false>(v);                // v[k] = X[2 lane + e + 64 k]
-  float2 g2[2] = {{0.f, 0.f}, {0.f, 0.f}};
-#pragma unroll
-  for (int k = 0; k < 32; ++k) {
-    const float2 w = cscale(v[k], Sq[64 * k]);
-    g2[k & 1] = cfma2(w, v[k], g2[k & 1]);
-    v[k] = w;
-  }
-  dft32<true>(v);  // over k: v[t] = U[2 lane + e][t]
-twiddle2048_inv(v, tw2, e, lane);  // conj W_2048^{(2 lane + e) t}
-  warp_transpose32(v, tr, lane);  // lane t: v[m] = U[2m + e][t]
-  dft32<true>(v);                 // v[r] = sum_m U[2m + e][t] W_32^{-r m}
-  if (e) {
-#pragma unroll
-    for (int r = 0; r < 32; ++r) zx[r * 32 + lane] = twiddle64<true>(v[r], r);
-  }
-  __syncthreads();
-  if (!e) {
-#pragma unroll
-    for (int r = 0; r < 32; ++r) {
-      const int n = lane + 32 * r;
-      if (live && (FULL || n < N)) col[n] = cadd(v[r], zx[r * 32 + lane]);
-    }
-  }
-  double gam = (double)(g2[0].x + g2[1].x) + (double)(g2[0].y + g2[1].y);
-  if (q != 0 && q != L / 2) gam *= 2.0;  // the other half of the Hermitian spectrum
-  if (!live) gam = 0.0;
-  if (gpart) {  // deterministic CTA reduction
-    for (int o = 16; o > 0; o >>= 1) gam += __shfl_xor_sync(0xffffffffu, gam, o);
-    if (lane == 0) red[warp] = gam;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double t = 0;
-      for (int i = 0; i < NWP; ++i) t += red[i];
-      gpart[(size_t)b * gridDim.x + blockIdx.x] = t;
-    }
-  }
+  extern __shared__ __align__(16) float2 pb2_smem[];
+  pass_b_2048_tile<FULL, PB2_COLS>(blockIdx.x, blockIdx.y, gridDim.x, N, T1, S, tw2, gpart, pb2_smem);
 }
 
 // ---------------------------------------------------------------- pass B, L = 512 (FP32)
@@ -624,7 +559,7 @@ static cudaError_t pass_b_L(int N, int B, cplx<T> *T1, const T *S, const cplx<T>
       const float2 *tw2 = tw2048_table();
       if (!tw2) return cudaErrorMemoryAllocation;
       const dim3 grid((L / 2 + 1 + PB2_COLS - 1) / PB2_COLS, B);
-      constexpr size_t sm = sizeof(float2) * (2 * PB2_COLS * 32 * 33 + PB2_COLS * 32 * 32);
+      constexpr size_t sm = pass_b_2048_smem<PB2_COLS>();
       cudaError_t e = set_smem(pass_b_2048_kernel<true>, sm);
       if (e == cudaSuccess) e = set_smem(pass_b_2048_kernel<false>, sm);
       if (e != cudaSuccess) return e;
