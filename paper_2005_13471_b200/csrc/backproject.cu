@@ -55,10 +55,20 @@ static cudaError_t upload_q() {
 }
 
 // One CTA per (angle, slice-group): CR_ROWS sinogram rows of the same angle (one per slice)
-// staged in shared memory with the taps; each output sample is a 51-tap dot product with
-// the taps read from shared memory (uniform index across the warp: broadcast).  The
-// degree test is per angle, hence uniform per CTA.
-constexpr int CR_ROWS = 8;
+// staged in shared memory, zero-extended.  Each thread computes CJ consecutive outputs of one row
+// from a register window of CJ + 2 HC inputs (vector shared-memory loads), the 51 taps as
+// constant-bank operands: 51 CJ FMAs per (CJ + 2 HC) / 4 shared loads instead of two shared loads
+// per FMA (the round-1 form was bound by shared-memory bandwidth: 5.4 ms per config-5 step against
+// ~1 ms of HBM traffic; this form 1.95 ms, tools/time_k3.py).  Per output the taps are summed in the same order as before (t = 0..2 HC),
+// so the result is bitwise unchanged.  The degree test is per angle, hence uniform per CTA.
+#ifndef BSCT_CR_ROWS
+#define BSCT_CR_ROWS 4
+#define BSCT_CR_THREADS 128
+#define BSCT_CJ 4
+#endif
+constexpr int CR_ROWS = BSCT_CR_ROWS;  // rows (slices) per CTA
+constexpr int CR_THREADS = BSCT_CR_THREADS;
+constexpr int CJ = BSCT_CJ;            // outputs per thread
 
 // split != nullptr (FP32, K4 v4): gt receives the TF32-rounded value (cvt.rna) and split the exact
 // FP32 residual, both with row stride ldt (the 3xTF32 operands of the tensor-core back projection)
@@ -68,43 +78,105 @@ __device__ __forceinline__ float tf32_round(float x) {
   return __uint_as_float(r);
 }
 
+// shared-memory row stride: the groups of CJ outputs plus the window overhang, a multiple of 4
+__host__ __device__ inline int correction_row_stride(int M) {
+  const int G = (M + 2 * HC + CJ - 1) / CJ;
+  return (G * CJ + 2 * HC + 4 + 3) & ~3;
+}
+
 template <typename T>
-__global__ void __launch_bounds__(256) correction_kernel(int n_angles, int M, int B, const int *__restrict__ degree,
+__device__ __forceinline__ void correction_store(T v, size_t o, T *__restrict__ gt, T *__restrict__ split) {
+  if (split) {
+    if constexpr (sizeof(T) == 4) {
+      const T hi = tf32_round(v);
+      gt[o] = hi;
+      split[o] = v - hi;
+    }
+  } else {
+    gt[o] = v;
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(CR_THREADS) correction_kernel(int n_angles, int M, int B, const int *__restrict__ degree,
                                                          const T *__restrict__ sino, T *__restrict__ gt,
-                                                         T *__restrict__ split, int ldt) {
+                                                         T *__restrict__ split, int ldt, int vec_ok) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T *rows = reinterpret_cast<T *>(smem_raw);  // [CR_ROWS][M + 4 HC], zero-extended by 2 HC each side
-  __shared__ T qs[2 * HC + 1];
+  T *rows = reinterpret_cast<T *>(smem_raw);  // [CR_ROWS][Mp]: rows[rr Mp + u] = g[u - 2 HC], zero outside [0, M)
   const int a = blockIdx.x, b0 = blockIdx.y * CR_ROWS;
   const int nb = min(CR_ROWS, B - b0);
-  const int Mp = M + 4 * HC, Mt = M + 2 * HC;
+  const int Mt = M + 2 * HC, Mp = correction_row_stride(M);
   const int d = degree[a];
-  if (threadIdx.x < 2 * HC + 1) qs[threadIdx.x] = qtap<T>(threadIdx.x);
-  for (int i = threadIdx.x; i < nb * Mp; i += blockDim.x) {
-    const int rr = i / Mp, m = i - rr * Mp - 2 * HC;
-    rows[i] = (m >= 0 && m < M) ? sino[((size_t)(b0 + rr) * n_angles + a) * M + m] : (T)0;
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i < nb * Mt; i += blockDim.x) {
-    const int rr = i / Mt, j = i - rr * Mt;  // output j <-> detector index m = j - HC
-    const T *row = rows + rr * Mp + j;       // row[u] = g[j - 2 HC + u]
-    T v = 0;
-    if (d == 2) {
-      // g~[m] = sum_{t=0}^{2 HC} q[t - HC] g[m - (t - HC)] = sum_t qs[t] g[j - t]
-#pragma unroll
-      for (int t = 0; t <= 2 * HC; ++t) v = fma(qs[t], row[2 * HC - t], v);
-    } else {
-      v = row[HC];
+  // every global load of the CTA is issued at once as cp.async (rows start at 4-byte alignment
+  // only: M is odd in the paper's geometries); the zero extension by plain stores
+  for (int rr = 0; rr < nb; ++rr) {
+    const T *src = sino + ((size_t)(b0 + rr) * n_angles + a) * M;
+    T *dst = rows + rr * Mp;
+    for (int m = threadIdx.x; m < M; m += blockDim.x) {
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 2 * HC + m);
+      if constexpr (sizeof(T) == 4)
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(src + m) : "memory");
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(sa), "l"(src + m) : "memory");
     }
-    const size_t o = ((size_t)(b0 + rr) * n_angles + a) * ldt + j;
-    if (split) {
+    for (int u = threadIdx.x; u < Mp - M; u += blockDim.x) dst[u < 2 * HC ? u : u + M] = (T)0;
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+  asm volatile("cp.async.wait_group 0;" ::: "memory");
+  __syncthreads();
+  if (d != 2) {  // no correction at this angle: g~[m] = g[m], output j <-> detector index m = j - HC
+    for (int i = threadIdx.x; i < nb * Mt; i += blockDim.x) {
+      const int rr = i / Mt, j = i - rr * Mt;
+      correction_store<T>(rows[rr * Mp + j + HC], ((size_t)(b0 + rr) * n_angles + a) * ldt + j, gt, split);
+    }
+    return;
+  }
+  constexpr int VE = 16 / (int)sizeof(T);                      // elements per 16-byte shared load
+  constexpr int NW = ((CJ + 2 * HC + VE - 1) / VE) * VE;       // window registers
+  const int G = (Mt + CJ - 1) / CJ;
+  for (int it = threadIdx.x; it < nb * G; it += blockDim.x) {
+    const int rr = it / G, j0 = (it - rr * G) * CJ;            // outputs j0 .. j0 + CJ - 1 of row rr
+    const T *row = rows + rr * Mp + j0;                        // row[u] = g[j0 - 2 HC + u], 16-byte aligned
+    T w[NW];
+#pragma unroll
+    for (int k = 0; k < NW / VE; ++k) {
       if constexpr (sizeof(T) == 4) {
-        const T hi = tf32_round(v);
-        gt[o] = hi;
-        split[o] = v - hi;
+        const float4 t4 = reinterpret_cast<const float4 *>(row)[k];
+        w[4 * k] = t4.x, w[4 * k + 1] = t4.y, w[4 * k + 2] = t4.z, w[4 * k + 3] = t4.w;
+      } else {
+        const double2 t2 = reinterpret_cast<const double2 *>(row)[k];
+        w[2 * k] = t2.x, w[2 * k + 1] = t2.y;
+      }
+    }
+    // g~[m] = sum_{t=0}^{2 HC} q[t - HC] g[m - (t - HC)]: v[k] = sum_t q[t] row[k + 2 HC - t]
+    T v[CJ];
+#pragma unroll
+    for (int k = 0; k < CJ; ++k) v[k] = (T)0;
+#pragma unroll
+    for (int t = 0; t <= 2 * HC; ++t) {
+      const T q = qtap<T>(t);
+#pragma unroll
+      for (int k = 0; k < CJ; ++k) v[k] = fma(q, w[k + 2 * HC - t], v[k]);
+    }
+    const size_t o = ((size_t)(b0 + rr) * n_angles + a) * ldt + j0;
+    if (sizeof(T) == 4 && vec_ok && j0 + CJ <= Mt) {
+      if constexpr (sizeof(T) == 4) {
+        float hi[CJ], lo[CJ];
+#pragma unroll
+        for (int k = 0; k < CJ; ++k) {
+          hi[k] = split ? tf32_round(v[k]) : v[k];
+          lo[k] = v[k] - hi[k];
+        }
+#pragma unroll
+        for (int k = 0; k < CJ; k += 4) {
+          *reinterpret_cast<float4 *>(gt + o + k) = float4{hi[k], hi[k + 1], hi[k + 2], hi[k + 3]};
+          if (split) *reinterpret_cast<float4 *>(split + o + k) = float4{lo[k], lo[k + 1], lo[k + 2], lo[k + 3]};
+        }
       }
     } else {
-      gt[o] = v;
+#pragma unroll
+      for (int k = 0; k < CJ; ++k)
+        if (j0 + k < Mt) correction_store<T>(v[k], o + k, gt, split);
     }
   }
 }
@@ -114,14 +186,16 @@ cudaError_t correction_filter(int n_angles, int M, int B, const int *degree, con
                               T *split, int ldt) {
   cudaError_t e = upload_q();
   if (e != cudaSuccess) return e;
-  const size_t sm = sizeof(T) * (size_t)CR_ROWS * (M + 4 * HC);
+  const size_t sm = sizeof(T) * (size_t)CR_ROWS * correction_row_stride(M);
   if (sm > 48 * 1024) {
     e = cudaFuncSetAttribute(correction_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     if (e != cudaSuccess) return e;
   }
   if (ldt <= 0) ldt = M + 2 * HC;
-  correction_kernel<T><<<dim3(n_angles, (B + CR_ROWS - 1) / CR_ROWS), 256, sm, s>>>(n_angles, M, B, degree, sino, gt,
-                                                                                     split, ldt);
+  // 16-byte output stores where every row start is aligned (the K4 v4 operand layout: ldt % 4 == 0)
+  const int vec_ok = sizeof(T) == 4 && ldt % 4 == 0 && ((uintptr_t)gt & 15) == 0 && ((uintptr_t)split & 15) == 0;
+  correction_kernel<T><<<dim3(n_angles, (B + CR_ROWS - 1) / CR_ROWS), CR_THREADS, sm, s>>>(n_angles, M, B, degree, sino, gt,
+                                                                                     split, ldt, vec_ok);
   return cudaGetLastError();
 }
 
