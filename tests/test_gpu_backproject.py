@@ -39,6 +39,26 @@ def test_correction_filter(cuda_lib, zeta, ly, dt):
             assert rel_l2(got[bi, a], ref) < tol(dt)
 
 
+@pytest.mark.parametrize("M,B,dt", [(5, 1, "f32"), (38, 5, "f32"), (39, 4, "f64"), (40, 7, "f32"), (53, 9, "f64"),
+                                    (725, 6, "f32"), (725, 3, "f64")])
+def test_correction_filter_tails(cuda_lib, M, B, dt):
+    """K3 v2 thread/CTA tiling (4 outputs per thread, 4 rows per CTA): every residue of M + 50 mod 4,
+    ragged last CTAs (B mod 4 != 0) and the config-5 row length, each row against the oracle."""
+    import torch
+    n = 6
+    g = geom(6, uniform(n), M, lambda_y=1.0, zeta=1.0)
+    sino = random_sinogram(M + B, B, n, M)
+    plan, _ = gpu_plan(cuda_lib, g, dt, max_batch=B)
+    gt = torch.full((B, n, M + 2 * H_CORR), float("nan"), dtype=plan.dtype, device="cuda")
+    cuda_lib.correction_filter(plan, to_dev(sino, dt), gt)
+    got = to_np(gt)
+    assert np.isfinite(got).all()
+    for bi in range(B):
+        for a, t in enumerate(g["angles"]):
+            ref = corrected_row(sino[bi, a], interpolation_degree(g, t))
+            assert rel_l2(got[bi, a], ref) < tol(dt)
+
+
 @pytest.mark.parametrize("N,n,M,ly,zeta,dt,B", [
     (1, 3, 5, 1.0, 0.0, "f32", 1), (4, 8, 9, 1.0, 1.0, "f64", 2), (7, 11, 15, 0.5, 0.5, "f32", 2),
     (16, 24, 33, 1.0, 0.0, "f32", 1), (16, 24, 23, 1.3, 1.7, "f64", 1), (33, 36, 49, 1.0, 1.5, "f32", 2),
