@@ -301,6 +301,19 @@ bsct_status gram_build_t(const bsct_geometry *g, int a0, int a1, T *taps, cudaSt
     while (i < n && (k == GRAM_NB || srt[i].first < edge)) ++i;
     bucket[k] = i;
   }
+  // angular density for K1's tile levels: the fullest pi / 16 window (with wrap) x 16; a set spread
+  // over [0, pi) keeps n, an angle shard (config 4: a wedge of the angle range) gets ~n pi / wedge
+  double n_dens = n;
+  {
+    const int W = GRAM_NB / 16;
+    int most = 0;
+    for (int k = 0; k < GRAM_NB; ++k) {
+      const int e = k + W;
+      const int c = e <= GRAM_NB ? bucket[e] - bucket[k] : (n - bucket[k]) + bucket[e - GRAM_NB];
+      most = std::max(most, c);
+    }
+    if (16.0 * most > 1.5 * n) n_dens = 16.0 * most;
+  }
   double *ang = nullptr;
   CU(gram_angles(dev, key, sorted, bucket, &ang));
   const int *bk = (const int *)(ang + n);
@@ -313,7 +326,7 @@ bsct_status gram_build_t(const bsct_geometry *g, int a0, int a1, T *taps, cudaSt
   tb.grec = (T *)((char *)mem + tb_bytes);
   CU(build_pp_tables<T>(ang, n, PP_GRAM, g->lambda_x, g->lambda_y, g->zeta_blur, tb, s));
   const double Hmax = (g->lambda_x * 1.4142135623730951 + g->zeta_blur) * (1.0 + 1e-12);
-  CU(gram_build_tiles<T>(N, g->lambda_x, n, tb.grec, bk, GRAM_NB, Hmax, dense, taps, s));
+  CU(gram_build_tiles<T>(N, g->lambda_x, n, n_dens, tb.grec, bk, GRAM_NB, Hmax, dense, taps, s));
   CU(cudaFreeAsync(mem, s));
   return BSCT_OK;
 }

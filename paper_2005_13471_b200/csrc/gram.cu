@@ -295,17 +295,19 @@ __global__ void __launch_bounds__(256) gram_tiles_kernel(int N, int n, const T *
 }
 
 template <typename T>
-cudaError_t gram_build_tiles(int N, double lx, int n, const T *rec, const int *bucket, int nb, double Hmax, bool dense,
-                             T *taps, cudaStream_t s) {
+cudaError_t gram_build_tiles(int N, double lx, int n, double n_dens, const T *rec, const int *bucket, int nb,
+                             double Hmax, bool dense, T *taps, cudaStream_t s) {
   const int D = 2 * N - 1;
   const int T16 = (D + 15) / 16, R16 = (N - 1) / 16 + 1;  // 16-tiles per side, tile rows up to the centre
-  // level radii (taps): about <= 64 angles per thread at every level (K1)
+  // level radii (taps): about <= 64 angles per thread at every level (K1).  n_dens: the
+  // angles per pi where the set is densest (= n for angles spread over [0, pi); an angle shard of
+  // config 4 packs its n angles into a wedge, whose taps see n_dens / n times more of them)
   const double hm = Hmax / lx;
   double f1 = 1.0, f2 = 1.0;  // BSCT_GRAM_R1 / BSCT_GRAM_R2: scale the level radii (experiments)
   if (const char *e = getenv("BSCT_GRAM_R1")) f1 = atof(e);
   if (const char *e = getenv("BSCT_GRAM_R2")) f2 = atof(e);
-  const double R1 = dense ? 0.0 : f1 * (23.0 + 2.0 * hm) * n / (3.14159265 * 64.0);
-  const double R2 = dense ? 0.0 : f2 * (11.3 + 2.0 * hm) * n / (3.14159265 * 4.0 * 64.0);
+  const double R1 = dense ? 0.0 : f1 * (23.0 + 2.0 * hm) * n_dens / (3.14159265 * 64.0);
+  const double R2 = dense ? 0.0 : f2 * (11.3 + 2.0 * hm) * n_dens / (3.14159265 * 4.0 * 64.0);
   auto square = [&](double R, int &a, int &b) {  // 16-tiles meeting |dk| <= R in both coordinates
     if (R <= 0) {
       a = b = 0;
@@ -347,9 +349,9 @@ cudaError_t gram_build_tiles(int N, double lx, int n, const T *rec, const int *b
   return cudaLaunchKernelEx(&cfg, gram_tiles_kernel<T, false>, N, n, rec, bucket, nb, hmf, lv, sc, taps);
 }
 
-template cudaError_t gram_build_tiles<float>(int, double, int, const float *, const int *, int, double, bool, float *,
-                                             cudaStream_t);
-template cudaError_t gram_build_tiles<double>(int, double, int, const double *, const int *, int, double, bool,
+template cudaError_t gram_build_tiles<float>(int, double, int, double, const float *, const int *, int, double, bool,
+                                             float *, cudaStream_t);
+template cudaError_t gram_build_tiles<double>(int, double, int, double, const double *, const int *, int, double, bool,
                                               double *, cudaStream_t);
 
 }  // namespace bsct

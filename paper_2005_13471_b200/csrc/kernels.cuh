@@ -54,10 +54,11 @@ cudaError_t build_pp_tables(const double *angles_dev, int n, int kind, double lx
 // K1 (gram.cu): taps[(2N-1)^2] = lx^4 sum_{a < n} M_a(lx <(-s_a, c_a), dk>) from the per-angle
 // Gram records (GramRec layout, written by K0 when PPTables::grec is set) of angles sorted by
 // t mod pi; bucket[k] (k = 0..nb) = number of sorted angles with (t mod pi) < k pi / nb;
-// Hmax >= max_t W_t / 2.  dense: every (tap, angle) pair (measurement mode).
+// Hmax >= max_t W_t / 2.  dense: every (tap, angle) pair (measurement mode).  n_dens: angles per pi
+// where the set is densest (n for a set spread over [0, pi); sizes the central tile levels).
 template <typename T>
-cudaError_t gram_build_tiles(int N, double lx, int n, const T *rec, const int *bucket, int nb, double Hmax, bool dense,
-                             T *taps, cudaStream_t s);
+cudaError_t gram_build_tiles(int N, double lx, int n, double n_dens, const T *rec, const int *bucket, int nb,
+                             double Hmax, bool dense, T *taps, cudaStream_t s);
 
 // K2 (normal.cu): S[q][p] = Re DFT2(E)[p][q] / L^2, work >= (L/2+1)*L complex
 template <typename T>
