@@ -1156,8 +1156,10 @@ namespace {
 
 int pipe_chunk(int B, bool host) {
   // host path: chunks overlap the PCIe copies with compute (measured e2e 132K -> 142K
-  // slice-iterations/s on config 5); device path: one chunk unless BSCT_PIPE_CHUNK is set
-  int c = host ? 256 : 0;
+  // slice-iterations/s on config 5, round 1); device path: one chunk unless BSCT_PIPE_CHUNK is set.
+  // 512: the quarter-chunk edges are then 128 slices = one full K4 v4 slice tile (round 2, config 5
+  // e2e per step: 128: 471.6, 256: 394.3, 384: 390.2, 512: 389.3, 768: 394.3, 1024: 393.6 ms)
+  int c = host ? 512 : 0;
   if (const char *e = getenv("BSCT_PIPE_CHUNK")) c = atoi(e);
   if (c <= 0 || c >= B) return B;  // one chunk: no pipelining
   return c;
