@@ -455,7 +455,10 @@ def roofline(per: dict, cfg, B: int, clk: dict, peaks: dict):
                                "hbm_frac": kernels["pass_b"]["frac_of_measured_hbm"] if "pass_b" in kernels else None,
                                "traffic": tb, "traffic_source": tsrc,
                                "note": "FLOP = 2 x 5 L log2 L per column (nominal radix-2 count); the FP32 "
-                                       "FMA peak is the same for FFMA and FFMA2 (profiles/r02/fma_peak.json)"}
+                                       "FMA peak is the same for FFMA and FFMA2 (profiles/r02/fma_peak.json); "
+                                       "executed: 916 FP32x2 instructions per column and lane, ncu "
+                                       "sm__pipe_fma_cycles_active 69-74% "
+                                       "(profiles/r02/v10/ncu_full_summary.txt, ncu_full_summary_pass_b.txt)"}
     for kk, kname in (("pass_a", "cg_pass_a_1024_kernel"), ("pass_c", "cg_pass_c_1024_kernel")):
         if kk in kernels:
             tb, tsrc = ncu_traffic(kname, B)
