@@ -221,7 +221,7 @@ bsct_status bsct_reconstruct(bsct_plan plan, const void *sino, void *x, int32_t 
  * [B][n_angles][n_det] to the device, back projects, runs `iters` iterations of
  * `solver`, copies x to x_host [B][N][N], and synchronises `stream`.  Host
  * buffers should be pinned for full PCIe bandwidth.  B <= max_batch.  Pipelined by slice
- * chunks (BSCT_PIPE_CHUNK, default 256): each chunk's H2D copy runs on a plan-owned stream
+ * chunks (BSCT_PIPE_CHUNK, default 512, first and last chunk a quarter of that): each chunk's H2D copy runs on a plan-owned stream
  * ahead of its back projection and its D2H copy after its solve, overlapping the kernels.
  */
 bsct_status bsct_reconstruct_host(bsct_plan plan, const void *sino_host, void *x_host, int32_t B, int32_t iters,
