@@ -303,7 +303,10 @@ cudaError_t gram_build_tiles(int N, double lx, int n, double n_dens, const T *re
   // angles per pi where the set is densest (= n for angles spread over [0, pi); an angle shard of
   // config 4 packs its n angles into a wedge, whose taps see n_dens / n times more of them)
   const double hm = Hmax / lx;
-  double f1 = 1.0, f2 = 1.0;  // BSCT_GRAM_R1 / BSCT_GRAM_R2: scale the level radii (experiments)
+  // BSCT_GRAM_R1 / BSCT_GRAM_R2: scale the level radii (experiments).  Level 1 reaches 1.5x further
+  // than the 64-angles-per-thread rule: config 5 31.0 -> 28.9 us, config 4 unchanged
+  // (profiles/r02/gram_r_sweep.txt)
+  double f1 = 1.5, f2 = 1.0;
   if (const char *e = getenv("BSCT_GRAM_R1")) f1 = atof(e);
   if (const char *e = getenv("BSCT_GRAM_R2")) f2 = atof(e);
   const double R1 = dense ? 0.0 : f1 * (23.0 + 2.0 * hm) * n_dens / (3.14159265 * 64.0);
