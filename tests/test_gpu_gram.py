@@ -28,6 +28,19 @@ def test_irregular_angles(cuda_lib):
     assert rel_l2(to_np(gpu_taps(cuda_lib, g, "f32")), gram_taps(g)) < 1e-5
 
 
+@pytest.mark.parametrize("dt", ["f32", "f64"])
+def test_clustered_angles(cuda_lib, dt):
+    """Angle sets packed into a narrow wedge (an angle shard of config 4, repeated views): K1 sizes
+    its central tile levels by the angular density, not by n; the taps still equal the oracle's."""
+    wedge = 0.4 + np.arange(120) * (np.pi / 8 / 120)   # 120 angles in a pi/8 wedge
+    repeated = np.concatenate([np.full(60, 1.1), [0.0, 2.0, 2.9]])
+    for ang in (wedge, repeated, np.concatenate([wedge, wedge + np.pi])):   # the last wraps mod pi
+        g = geom(48, ang, 97, zeta=1.0)
+        G = to_np(gpu_taps(cuda_lib, g, dt))
+        assert rel_l2(G, gram_taps(g)) < tol(dt)
+        assert np.array_equal(G, G[::-1, ::-1])
+
+
 def test_axis_and_45deg(cuda_lib):
     g = geom(6, [0.0, np.pi / 2, np.pi / 4], 13, zeta=0.0)
     assert rel_l2(to_np(gpu_taps(cuda_lib, g, "f64")), gram_taps(g)) < 1e-12
